@@ -1,0 +1,249 @@
+/* pbfs.h — C ABI of the B200-native level-synchronous BFS (arXiv 2503.00430).
+ *
+ * This is the drop-in boundary the reference's C++ entry points reach the GPU
+ * through. Plain C types only: pointers, sizes, status codes. No torch, no
+ * C++ types. Every entry point cites the reference interface it replaces
+ * (paths relative to the reference's proj/ directory).
+ *
+ * Threading: a pbfs_graph is immutable after creation; pbfs_bfs* calls on one
+ * handle are serialised by a per-handle mutex (its traversal scratch lives in
+ * the handle); distinct handles may run concurrently ("safe to
+ * invoke concurrently on distinct output buffers").
+ *
+ * Errors: every call returns a pbfs_status; pbfs_last_error() holds a
+ * thread-local message. The status values map one-to-one onto the reference
+ * exception classes (core/include/parbfs/types.hpp:25-68).
+ */
+#ifndef PBFS_H
+#define PBFS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBFS_ABI_VERSION 1u
+#define PBFS_UNREACHED 0xFFFFFFFFu /* == parbfs::kUnreached (types.hpp:19) == int32 -1 */
+
+typedef enum pbfs_status {
+  PBFS_OK = 0,
+  PBFS_E_INPUT = 1,       /* parbfs::InputError    (types.hpp:33-36) */
+  PBFS_E_CONFIG = 2,      /* parbfs::ConfigError   (types.hpp:39-42) */
+  PBFS_E_FORMAT = 3,      /* parbfs::FormatError   (types.hpp:45-48) */
+  PBFS_E_CAPACITY = 4,    /* parbfs::CapacityError (types.hpp:53-56) */
+  PBFS_E_DEVICE = 5,      /* CUDA runtime failure  -> parbfs::Error  */
+  PBFS_E_COMM = 6,        /* collective failure    -> parbfs::Error  */
+  PBFS_E_METRIC = 7,      /* parbfs::MetricError   (types.hpp:65-68) */
+  PBFS_E_CORRECTNESS = 8  /* parbfs::CorrectnessError (types.hpp:59-62) */
+} pbfs_status;
+
+/* parbfs::KernelVariant (core/include/parbfs/kernel_config.hpp:13-22),
+ * same numbering. The GPU implements CONVENTIONAL, NONATOMIC, HYBRID,
+ * HYBRID_BEAMER and VISITED_INLINE; SERIAL, VISITED_DEFERRED and
+ * PERIODIC_FLUSH are CPU-only artefacts and are rejected with PBFS_E_CONFIG. */
+typedef enum pbfs_variant {
+  PBFS_SERIAL = 0,
+  PBFS_CONVENTIONAL = 1,     /* top-down, atomicCAS claim on dist (kernels.cpp:282-290) */
+  PBFS_NONATOMIC = 2,        /* top-down, plain same-value dist stores (kernels.cpp:291-301) */
+  PBFS_HYBRID = 3,           /* TD/BU by the 5 % frontier-size rule (kernels.cpp:494-497) */
+  PBFS_HYBRID_BEAMER = 4,    /* TD/BU by Beamer alpha/beta (kernels.cpp:498-511) */
+  PBFS_VISITED_INLINE = 5,   /* hybrid, visited-bitmap claim, inline dist (kernels.cpp:302-320) */
+  PBFS_VISITED_DEFERRED = 6,
+  PBFS_PERIODIC_FLUSH = 7
+} pbfs_variant;
+
+typedef enum pbfs_phase { PBFS_TOP_DOWN = 0, PBFS_BOTTOM_UP = 1 } pbfs_phase;
+
+/* Borrowed host view of a CSR graph, layout-compatible with parbfs::CsrGraph
+ * (core/include/parbfs/csr_graph.hpp:20-46): row_offsets has vertex_count+1
+ * entries of offset_bytes (8 = parbfs::EdgeOffset, or 4), column_indices has
+ * edge_count u32 entries sorted per row. Only read during the call. */
+typedef struct pbfs_csr {
+  uint64_t vertex_count;
+  uint64_t edge_count;
+  const void* row_offsets;
+  const uint32_t* column_indices;
+  uint32_t offset_bytes;
+  uint32_t symmetric;
+} pbfs_csr;
+
+/* parbfs::KernelConfig (kernel_config.hpp:38-70). worker_count and
+ * flush_capacity are validated exactly like parbfs::validate
+ * (kernel_config.cpp:9-26) but have no GPU meaning. */
+typedef struct pbfs_config {
+  uint32_t variant;
+  uint32_t worker_count;
+  double hybrid_threshold_fraction; /* (0, 1], default 0.05 */
+  double alpha;                     /* > 0, default 15 */
+  double beta;                      /* > 0, default 18 */
+  uint64_t flush_capacity;          /* >= 1, default 4096 */
+  uint32_t force_top_down_only;
+  uint32_t validate_same_value_stores;
+  uint32_t racy_visited_claim;
+  uint32_t reserved;
+} pbfs_config;
+
+/* parbfs::LevelRecord (core/include/parbfs/trace.hpp:26-35). */
+typedef struct pbfs_level {
+  uint32_t depth;
+  uint32_t phase; /* pbfs_phase */
+  uint64_t frontier_size;
+  uint64_t distinct_size;
+  uint64_t duplicate_count;
+  uint64_t edges_examined;
+  uint64_t flush_events;
+  int64_t elapsed_ns; /* device %globaltimer span of the iteration */
+} pbfs_level;
+
+/* Whole-run figures (parbfs::TraversalTrace, trace.hpp:37-48). */
+typedef struct pbfs_run_info {
+  uint32_t levels;                /* records produced (may exceed levels_cap) */
+  uint32_t bottom_up_levels;
+  uint64_t reached;               /* sum of distinct sizes = reachable set */
+  uint64_t same_value_violations; /* under validate_same_value_stores */
+  uint64_t edges_examined;
+  float device_ms;                /* CUDA-event time of the traversal kernel */
+  uint32_t reserved;
+} pbfs_run_info;
+
+typedef struct pbfs_graph_options {
+  int32_t device;               /* CUDA ordinal */
+  uint32_t device_offset_bytes; /* 0 = auto (4 if edge_count < 2^31 else 8), 4 or 8 */
+} pbfs_graph_options;
+
+typedef struct pbfs_graph_info {
+  uint64_t vertex_count;
+  uint64_t edge_count;
+  uint64_t max_degree;
+  uint64_t device_bytes; /* HBM held by the handle (graph + scratch) */
+  uint32_t device_offset_bytes;
+  uint32_t symmetric;
+  int32_t device;
+  uint32_t grid_blocks; /* persistent traversal grid (SMs x resident CTAs) */
+  uint32_t block_threads;
+  uint32_t reserved;
+} pbfs_graph_info;
+
+typedef struct pbfs_graph pbfs_graph;
+
+/* ---- version / errors --------------------------------------------------- */
+uint32_t pbfs_abi_version(void);
+const char* pbfs_last_error(void);
+const char* pbfs_status_string(pbfs_status status);
+
+/* Fills cfg with parbfs::KernelConfig{} defaults (kernel_config.hpp:38-70). */
+void pbfs_config_init(pbfs_config* cfg);
+
+/* parbfs::validate (kernel_config.cpp:9-26) plus the GPU variant check. */
+pbfs_status pbfs_config_validate(const pbfs_config* cfg);
+
+/* ---- device graph -------------------------------------------------------- */
+/* Uploads a host CSR to HBM and allocates the per-handle traversal scratch.
+ * Replaces the parbfs::Engine constructor's allocations (kernels.cpp:72-102),
+ * paid once per graph instead of once per BFS. Validates the CSR invariants
+ * (validate_csr, csr_graph.cpp:68-113): PBFS_E_FORMAT on a broken graph. */
+pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt,
+                              pbfs_graph** out);
+pbfs_status pbfs_graph_destroy(pbfs_graph* g);
+pbfs_status pbfs_graph_get_info(const pbfs_graph* g, pbfs_graph_info* info);
+
+/* ---- traversal ----------------------------------------------------------- */
+/* One BFS end to end: the reference's run_bfs / bfs_* call
+ * (core/include/parbfs/kernels.hpp:34-81; kernels.cpp:586-691) with the
+ * parbfs::BfsResult written into caller buffers.
+ *   dist_host: vertex_count u32 (int32 -1 = unreached), may be NULL (results
+ *              then stay on the device: pbfs_graph_device_dist).
+ *   levels:    up to levels_cap parbfs::LevelRecord rows, may be NULL.
+ *   info:      may be NULL.
+ * Applies the reference's checks first: check_source (kernels.cpp:562-568,
+ * PBFS_E_INPUT) and check_symmetric for direction-switching variants
+ * (kernels.cpp:570-577, PBFS_E_INPUT). Frontier overflow -> PBFS_E_CAPACITY
+ * (frontier.hpp:88-93). Synchronous. */
+pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
+                     uint32_t* dist_host, pbfs_level* levels, uint32_t levels_cap,
+                     pbfs_run_info* info);
+
+/* Enqueue-only traversal on a caller stream (cudaStream_t passed as void*,
+ * NULL = the handle's stream); distances stay in HBM. No trace, no host sync.
+ * For benchmark loops that keep inputs resident. pbfs_graph_sync() collects
+ * the status (capacity overflow is reported there). */
+pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
+                           void* stream);
+pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream);
+
+/* Device pointer of the distance array written by the last traversal. */
+pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev);
+
+/* Reached-component figures of the last traversal, computed on the device:
+ * N_r and A_r = sum of reached degrees (SURVEY.md §8(d) metric inputs). */
+pbfs_status pbfs_graph_component(pbfs_graph* g, uint64_t* n_reached,
+                                 uint64_t* arcs_reached);
+
+/* Pinned host buffers for zero-staging device<->host copies. */
+pbfs_status pbfs_host_alloc(size_t bytes, void** out);
+pbfs_status pbfs_host_free(void* p);
+
+/* ---- host graph construction (core/include/parbfs/{generator,csr_graph,
+ *      graph_stats,graph_io}.hpp) -------------------------------------------- */
+typedef struct pbfs_host_csr pbfs_host_csr; /* owns u64 offsets + u32 columns */
+
+typedef enum pbfs_gen_kind {
+  PBFS_GEN_UNIFORM = 0,   /* GeneratorKind::UniformRandom (generator.cpp:60-66) */
+  PBFS_GEN_KRONECKER = 1, /* GeneratorKind::Kronecker     (generator.cpp:67-89) */
+  PBFS_GEN_MESH = 2       /* config-3 road-like mesh (new) */
+} pbfs_gen_kind;
+
+typedef struct pbfs_gen_spec {
+  uint32_t kind;        /* pbfs_gen_kind */
+  uint32_t scale;       /* n = 2^scale (uniform / Kronecker) */
+  uint32_t edge_factor; /* samples = edge_factor * n */
+  uint32_t drop_self_loops; /* 1 = BASELINE semantics, 0 = reference semantics */
+  uint64_t seed;
+  uint32_t mesh_side;      /* mesh: side x side grid */
+  uint32_t mesh_radius;    /* mesh: shortcut Manhattan radius (32) */
+  double mesh_keep;        /* mesh: edge keep probability (0.9) */
+  uint64_t mesh_shortcuts; /* mesh: shortcut count (round(0.001 n)) */
+  uint32_t threads;        /* host threads for the builder, 0 = all */
+  uint32_t reserved;
+} pbfs_gen_spec;
+
+/* parbfs::generate (generator.cpp:41-92): the same mt19937_64 draw sequence
+ * bit for bit, then build_csr(symmetrize=true). */
+pbfs_status pbfs_generate(const pbfs_gen_spec* spec, pbfs_host_csr** out);
+
+/* parbfs::build_csr (csr_graph.cpp:11-55): range check, optional symmetrize,
+ * per-row sort + dedup; drop_self_loops applies BASELINE's removal. pairs is
+ * npairs interleaved (src, dst) u32. Parallel 2-pass bucketed counting sort. */
+pbfs_status pbfs_build_csr(const uint32_t* pairs, uint64_t npairs, uint64_t vertex_count,
+                           uint32_t symmetrize, uint32_t drop_self_loops, uint32_t threads,
+                           pbfs_host_csr** out);
+
+/* View (borrowed for the lifetime of the handle) with 8-byte offsets. */
+pbfs_status pbfs_host_csr_view(const pbfs_host_csr* h, pbfs_csr* view);
+pbfs_status pbfs_host_csr_free(pbfs_host_csr* h);
+
+/* parbfs::compute_stats (graph_stats.cpp:9-25). */
+typedef struct pbfs_stats {
+  uint64_t vertex_count;
+  uint64_t edge_count;
+  double average_degree;
+  uint64_t max_degree;
+  uint32_t large_diameter; /* GraphCategory::LargeDiameter iff avg < threshold */
+  uint32_t reserved;
+} pbfs_stats;
+pbfs_status pbfs_compute_stats(const pbfs_csr* csr, double threshold, pbfs_stats* out);
+
+/* bfsbench pick_sources (tools/bfsbench.cpp:206-235). */
+pbfs_status pbfs_pick_sources(const pbfs_csr* csr, uint32_t count, uint64_t seed,
+                              uint32_t* out);
+
+/* CSR1 binary format (core/src/graph_io.cpp:70-119). */
+pbfs_status pbfs_save_csr1(const pbfs_csr* csr, const char* path);
+pbfs_status pbfs_load_csr1(const char* path, pbfs_host_csr** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBFS_H */

@@ -1,0 +1,533 @@
+// Device runtime behind include/pbfs.h: graph residency in HBM, the
+// persistent traversal launch, trace/result copies, error mapping.
+//
+// Replaces, per reference file:
+//   kernels.cpp:72-126  Engine ctor/run   -> pbfs_graph_create (once per graph)
+//                                            + one cooperative launch per BFS
+//   kernels.cpp:562-577 check_source/check_symmetric -> pbfs_bfs prologue
+//   kernels.cpp:586-655 bfs_* wrappers     -> variant -> (claim, policy) map
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "pbfs_internal.h"
+#include "pbfs_kernels.cuh"
+
+namespace pbfs {
+const char* last_error_cstr();
+}
+
+using namespace pbfs;
+using namespace pbfs::dev;
+
+struct pbfs_graph {
+  std::mutex mu;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t n = 0, m = 0, max_degree = 0;
+  uint32_t offb = 8;
+  bool symmetric = false;
+  uint32_t words = 0;
+  void* rowptr = nullptr;
+  uint32_t* col = nullptr;
+  uint32_t* init_mask = nullptr;
+  uint32_t* dist = nullptr;
+  uint32_t* visited = nullptr;
+  uint32_t* bm[2] = {nullptr, nullptr};
+  uint32_t* queue[2] = {nullptr, nullptr};
+  HeavyItem* heavy = nullptr;
+  Ctl* ctl = nullptr;
+  pbfs_level* records = nullptr;
+  unsigned long long* comp = nullptr;
+  uint32_t rec_cap = 0;
+  uint64_t qcap = 0, heavy_cap = 0;
+  int grid = 0;
+  uint64_t device_bytes = 0;
+  std::vector<void*> allocs;
+  bool poisoned = false;  // a launch failed; ctl must be reset
+};
+
+namespace {
+
+pbfs_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky non-fatal state
+  return fail(PBFS_E_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PBFS_CUDA(call, what)                 \
+  do {                                        \
+    cudaError_t _e = (call);                  \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+template <typename T>
+pbfs_status dalloc(pbfs_graph* g, T** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PBFS_E_CAPACITY, "cudaMalloc of " + std::to_string(bytes) +
+                                     " bytes failed: " + cudaGetErrorString(e));
+  }
+  g->allocs.push_back(q);
+  g->device_bytes += bytes;
+  *p = static_cast<T*>(q);
+  return PBFS_OK;
+}
+
+void release(pbfs_graph* g) {
+  if (!g) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->device);
+  for (void* p : g->allocs) cudaFree(p);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  cudaSetDevice(prev);
+  delete g;
+}
+
+struct Launch {
+  int claim;
+  int policy;
+};
+
+pbfs_status map_variant(const pbfs_config* c, bool* hybrid_like, Launch* out) {
+  switch (c->variant) {
+    case PBFS_CONVENTIONAL:
+      *out = {kClaimCas, kPolicyTopDown};
+      *hybrid_like = false;
+      return PBFS_OK;
+    case PBFS_NONATOMIC:
+      *out = {kClaimPlain, kPolicyTopDown};
+      *hybrid_like = false;
+      return PBFS_OK;
+    case PBFS_HYBRID:
+    case PBFS_VISITED_INLINE:
+      *out = {kClaimBitmap, c->force_top_down_only ? kPolicyTopDown : kPolicyFraction};
+      *hybrid_like = true;
+      return PBFS_OK;
+    case PBFS_HYBRID_BEAMER:
+      *out = {kClaimBitmap, c->force_top_down_only ? kPolicyTopDown : kPolicyBeamer};
+      *hybrid_like = true;
+      return PBFS_OK;
+    case PBFS_SERIAL:
+      return fail(PBFS_E_CONFIG, "the serial variant is the CPU oracle, not a GPU kernel");
+    case PBFS_VISITED_DEFERRED:
+    case PBFS_PERIODIC_FLUSH:
+      return fail(PBFS_E_CONFIG,
+                  "visited-deferred and periodic-flush are CPU cache/memory artefacts "
+                  "with no GPU kernel (SURVEY.md §2)");
+    default:
+      return fail(PBFS_E_CONFIG, "unknown kernel variant");
+  }
+}
+
+template <int C, typename OffT>
+cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, int policy,
+                         cudaStream_t s) {
+  Params<OffT> p;
+  p.rowptr = static_cast<const OffT*>(g->rowptr);
+  p.col = g->col;
+  p.dist = g->dist;
+  p.visited = g->visited;
+  p.bm[0] = g->bm[0];
+  p.bm[1] = g->bm[1];
+  p.init_mask = g->init_mask;
+  p.queue[0] = g->queue[0];
+  p.queue[1] = g->queue[1];
+  p.heavy = g->heavy;
+  p.ctl = g->ctl;
+  p.records = g->records;
+  p.qcap = g->qcap;
+  p.heavy_cap = g->heavy_cap;
+  p.n = g->n;
+  p.m = g->m;
+  p.max_degree = g->max_degree;
+  p.words = g->words;
+  p.rec_cap = g->rec_cap;
+  p.source = source;
+  p.policy = policy;
+  p.validate = cfg->validate_same_value_stores ? 1 : 0;
+  p.threshold = cfg->hybrid_threshold_fraction;
+  p.alpha = cfg->alpha;
+  p.beta = cfg->beta;
+  void* args[] = {&p};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&bfs_persistent<C, OffT>),
+                                     dim3(g->grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, const Launch& l,
+                   cudaStream_t s) {
+  const bool wide = g->offb == 8;
+  switch (l.claim) {
+    case kClaimCas:
+      return wide ? launch_typed<kClaimCas, unsigned long long>(g, source, cfg, l.policy, s)
+                  : launch_typed<kClaimCas, uint32_t>(g, source, cfg, l.policy, s);
+    case kClaimPlain:
+      return wide ? launch_typed<kClaimPlain, unsigned long long>(g, source, cfg, l.policy, s)
+                  : launch_typed<kClaimPlain, uint32_t>(g, source, cfg, l.policy, s);
+    default:
+      return wide ? launch_typed<kClaimBitmap, unsigned long long>(g, source, cfg, l.policy, s)
+                  : launch_typed<kClaimBitmap, uint32_t>(g, source, cfg, l.policy, s);
+  }
+}
+
+template <typename OffT>
+int occupancy_for(int claim) {
+  int blocks = 0;
+  const void* fn = claim == kClaimCas     ? reinterpret_cast<const void*>(&bfs_persistent<kClaimCas, OffT>)
+                   : claim == kClaimPlain ? reinterpret_cast<const void*>(&bfs_persistent<kClaimPlain, OffT>)
+                                          : reinterpret_cast<const void*>(&bfs_persistent<kClaimBitmap, OffT>);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0);
+  return blocks;
+}
+
+pbfs_status prologue(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, Launch* l) {
+  if (!g || !cfg) return fail(PBFS_E_INPUT, "null argument");
+  pbfs_status st = pbfs_config_validate(cfg);
+  if (st != PBFS_OK) return st;
+  bool hybrid_like = false;
+  st = map_variant(cfg, &hybrid_like, l);
+  if (st != PBFS_OK) return st;
+  if (source >= g->n) {
+    return fail(PBFS_E_INPUT, "source vertex " + std::to_string(source) +
+                                  " is out of range for a graph with " + std::to_string(g->n) +
+                                  " vertices");
+  }
+  if (hybrid_like && !cfg->force_top_down_only && !g->symmetric) {
+    return fail(PBFS_E_INPUT,
+                "direction-switching traversal reads each adjacency list as in-edges, which "
+                "requires a symmetric graph; symmetrize the input or force the top-down-only "
+                "path");
+  }
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  if (g->poisoned) {
+    PBFS_CUDA(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream), "reset control block");
+    g->poisoned = false;
+  }
+  return PBFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t pbfs_abi_version(void) { return PBFS_ABI_VERSION; }
+const char* pbfs_last_error(void) { return pbfs::last_error_cstr(); }
+
+const char* pbfs_status_string(pbfs_status s) {
+  switch (s) {
+    case PBFS_OK: return "ok";
+    case PBFS_E_INPUT: return "input error";
+    case PBFS_E_CONFIG: return "config error";
+    case PBFS_E_FORMAT: return "format error";
+    case PBFS_E_CAPACITY: return "capacity error";
+    case PBFS_E_DEVICE: return "device error";
+    case PBFS_E_COMM: return "communication error";
+    case PBFS_E_METRIC: return "metric error";
+    case PBFS_E_CORRECTNESS: return "correctness error";
+  }
+  return "unknown status";
+}
+
+void pbfs_config_init(pbfs_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->variant = PBFS_CONVENTIONAL;
+  c->worker_count = 1;
+  c->hybrid_threshold_fraction = 0.05;
+  c->alpha = 15.0;
+  c->beta = 18.0;
+  c->flush_capacity = 4096;
+}
+
+// kernel_config.cpp:9-26
+pbfs_status pbfs_config_validate(const pbfs_config* c) {
+  if (!c) return fail(PBFS_E_INPUT, "null config");
+  if (c->worker_count < 1) return fail(PBFS_E_CONFIG, "worker count must be at least 1");
+  if (!(c->hybrid_threshold_fraction > 0.0) || c->hybrid_threshold_fraction > 1.0) {
+    return fail(PBFS_E_CONFIG, "hybrid threshold fraction must be in (0, 1]");
+  }
+  if (!(c->alpha > 0.0)) return fail(PBFS_E_CONFIG, "alpha must be positive");
+  if (!(c->beta > 0.0)) return fail(PBFS_E_CONFIG, "beta must be positive");
+  if (c->flush_capacity < 1) return fail(PBFS_E_CONFIG, "flush capacity must be at least 1");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt,
+                              pbfs_graph** out) {
+  if (!csr || !out) return fail(PBFS_E_INPUT, "null argument");
+  const unsigned threads = resolve_threads(0);
+  pbfs_status st = validate_csr_view(csr, threads);
+  if (st != PBFS_OK) return st;
+  const uint64_t n = csr->vertex_count, m = csr->edge_count;
+  uint32_t offb = opt ? opt->device_offset_bytes : 0;
+  if (offb == 0) offb = m < (1ull << 31) ? 4 : 8;
+  if (offb != 4 && offb != 8) return fail(PBFS_E_CONFIG, "device offset width must be 0, 4 or 8");
+  if (offb == 4 && m > 0x7fffffffULL) {
+    return fail(PBFS_E_CAPACITY, "edge count " + std::to_string(m) + " needs 64-bit offsets");
+  }
+  int device = opt ? opt->device : 0;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(PBFS_E_DEVICE, "no CUDA device available: the BFS kernels need a B200 "
+                               "(there is no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev) return fail(PBFS_E_CONFIG, "device ordinal out of range");
+
+  auto* g = new (std::nothrow) pbfs_graph;
+  if (!g) return fail(PBFS_E_CAPACITY, "host allocation failed");
+  g->device = device;
+  g->n = n;
+  g->m = m;
+  g->offb = offb;
+  g->symmetric = csr->symmetric != 0;
+  // Host-side per-graph facts: max degree, heavy-item capacity, the
+  // zero-degree mask that lets bottom-up skip isolated vertices.
+  g->words = static_cast<uint32_t>(((n + 31) / 32 + kGroupWords - 1) / kGroupWords * kGroupWords);
+  if (g->words == 0) g->words = kGroupWords;
+  std::vector<uint32_t> mask(g->words, 0);
+  {
+    std::vector<uint64_t> mx(threads, 0), hc(threads, 0);
+    parallel_for_threads(threads, [&](unsigned t) {
+      const uint64_t b = n * t / threads, en = n * (t + 1) / threads;
+      for (uint64_t v = b; v < en; ++v) {
+        const uint64_t d = csr_offset(csr, v + 1) - csr_offset(csr, v);
+        mx[t] = std::max(mx[t], d);
+        if (d > kHeavyDeg) hc[t] += (d + kChunk - 1) / kChunk;
+      }
+    });
+    for (unsigned t = 0; t < threads; ++t) {
+      g->max_degree = std::max(g->max_degree, mx[t]);
+      g->heavy_cap += hc[t];
+    }
+    if (g->symmetric) {
+      for (uint64_t v = 0; v < n; ++v) {
+        if (csr_offset(csr, v + 1) == csr_offset(csr, v)) mask[v >> 5] |= 1u << (v & 31);
+      }
+    }
+    for (uint64_t v = n; v < static_cast<uint64_t>(g->words) * 32; ++v) mask[v >> 5] |= 1u << (v & 31);
+  }
+  g->qcap = n + g->max_degree;
+  g->rec_cap = static_cast<uint32_t>(std::min<uint64_t>(n + 1, 1u << 20));
+
+  int prev = 0;
+  cudaGetDevice(&prev);
+  auto bail = [&](pbfs_status s2) {
+    release(g);
+    cudaSetDevice(prev);
+    return s2;
+  };
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return bail(cuda_fail(e, "cudaSetDevice"));
+  if ((e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaStreamCreate"));
+  if ((e = cudaEventCreate(&g->ev0)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  if ((e = cudaEventCreate(&g->ev1)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+
+  const size_t wbytes = static_cast<size_t>(g->words) * 4;
+  if ((st = dalloc(g, &g->rowptr, (n + 1) * offb)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->col, m * 4)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->init_mask, wbytes)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->dist, ((n + 3) / 4) * 16)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->visited, wbytes)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->bm[0], wbytes)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->bm[1], wbytes)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->queue[0], g->qcap * 4)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->queue[1], g->qcap * 4)) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->heavy, std::max<uint64_t>(g->heavy_cap, 1) * sizeof(HeavyItem))) != PBFS_OK)
+    return bail(st);
+  if ((st = dalloc(g, &g->ctl, sizeof(Ctl))) != PBFS_OK) return bail(st);
+  if ((st = dalloc(g, &g->records, static_cast<size_t>(g->rec_cap) * sizeof(pbfs_level))) != PBFS_OK)
+    return bail(st);
+  if ((st = dalloc(g, &g->comp, 2 * sizeof(unsigned long long))) != PBFS_OK) return bail(st);
+
+  // Offsets: upload as-is when the widths match, else narrow on the host.
+  if (offb == csr->offset_bytes) {
+    if ((e = cudaMemcpy(g->rowptr, csr->row_offsets, (n + 1) * offb, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return bail(cuda_fail(e, "upload offsets"));
+  } else {
+    std::vector<uint8_t> tmp((n + 1) * offb);
+    for (uint64_t v = 0; v <= n; ++v) {
+      const uint64_t o = csr_offset(csr, v);
+      if (offb == 4) {
+        reinterpret_cast<uint32_t*>(tmp.data())[v] = static_cast<uint32_t>(o);
+      } else {
+        reinterpret_cast<uint64_t*>(tmp.data())[v] = o;
+      }
+    }
+    if ((e = cudaMemcpy(g->rowptr, tmp.data(), tmp.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return bail(cuda_fail(e, "upload offsets"));
+  }
+  if (m && (e = cudaMemcpy(g->col, csr->column_indices, m * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return bail(cuda_fail(e, "upload columns"));
+  if ((e = cudaMemcpy(g->init_mask, mask.data(), wbytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return bail(cuda_fail(e, "upload mask"));
+  if ((e = cudaMemset(g->ctl, 0, sizeof(Ctl))) != cudaSuccess) return bail(cuda_fail(e, "memset ctl"));
+
+  // Persistent grid: every SM x resident CTAs of the widest instantiation.
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(cuda_fail(e, "props"));
+  int occ = 1 << 30;
+  for (int c = 0; c < 3; ++c) {
+    occ = std::min(occ, offb == 8 ? occupancy_for<unsigned long long>(c) : occupancy_for<uint32_t>(c));
+  }
+  if (occ < 1) return bail(fail(PBFS_E_DEVICE, "traversal kernel cannot be resident"));
+  g->grid = prop.multiProcessorCount * occ;
+  cudaSetDevice(prev);
+  *out = g;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_destroy(pbfs_graph* g) {
+  release(g);
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_get_info(const pbfs_graph* g, pbfs_graph_info* info) {
+  if (!g || !info) return fail(PBFS_E_INPUT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->vertex_count = g->n;
+  info->edge_count = g->m;
+  info->max_degree = g->max_degree;
+  info->device_bytes = g->device_bytes;
+  info->device_offset_bytes = g->offb;
+  info->symmetric = g->symmetric;
+  info->device = g->device;
+  info->grid_blocks = static_cast<uint32_t>(g->grid);
+  info->block_threads = kThreads;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uint32_t* dist_host,
+                     pbfs_level* levels, uint32_t levels_cap, pbfs_run_info* info) {
+  if (!g) return fail(PBFS_E_INPUT, "null graph");
+  std::lock_guard<std::mutex> lock(g->mu);
+  Launch l;
+  pbfs_status st = prologue(g, source, cfg, &l);
+  if (st != PBFS_OK) return st;
+  cudaError_t e;
+  PBFS_CUDA(cudaEventRecord(g->ev0, g->stream), "event record");
+  if ((e = launch(g, source, cfg, l, g->stream)) != cudaSuccess) {
+    g->poisoned = true;
+    return cuda_fail(e, "traversal launch");
+  }
+  PBFS_CUDA(cudaEventRecord(g->ev1, g->stream), "event record");
+  Ctl ctl;
+  PBFS_CUDA(cudaMemcpyAsync(&ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream), "read control");
+  if ((e = cudaStreamSynchronize(g->stream)) != cudaSuccess) {
+    g->poisoned = true;
+    return cuda_fail(e, "traversal");
+  }
+  if (ctl.overflow) {
+    g->poisoned = true;
+    return fail(PBFS_E_CAPACITY, "dense frontier overflow");
+  }
+  if (dist_host) {
+    PBFS_CUDA(cudaMemcpy(dist_host, g->dist, g->n * 4, cudaMemcpyDeviceToHost), "read distances");
+  }
+  const uint32_t nrec = std::min<uint32_t>(ctl.levels, g->rec_cap);
+  if (levels && levels_cap) {
+    const uint32_t k = std::min(nrec, levels_cap);
+    PBFS_CUDA(cudaMemcpy(levels, g->records, k * sizeof(pbfs_level), cudaMemcpyDeviceToHost), "read trace");
+  }
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->levels = ctl.levels;
+    info->bottom_up_levels = ctl.bu_levels;
+    info->reached = ctl.reached;
+    info->same_value_violations = ctl.violations;
+    info->edges_examined = ctl.edges;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g->ev0, g->ev1);
+    info->device_ms = ms;
+  }
+  if (ctl.levels > g->rec_cap && levels) {
+    return fail(PBFS_E_CAPACITY, "traversal depth exceeds the device trace capacity");
+  }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, void* stream) {
+  if (!g) return fail(PBFS_E_INPUT, "null graph");
+  std::lock_guard<std::mutex> lock(g->mu);
+  Launch l;
+  pbfs_status st = prologue(g, source, cfg, &l);
+  if (st != PBFS_OK) return st;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  cudaError_t e = launch(g, source, cfg, l, s);
+  if (e != cudaSuccess) {
+    g->poisoned = true;
+    return cuda_fail(e, "traversal launch");
+  }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream) {
+  if (!g) return fail(PBFS_E_INPUT, "null graph");
+  std::lock_guard<std::mutex> lock(g->mu);
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    g->poisoned = true;
+    return cuda_fail(e, "traversal");
+  }
+  unsigned int overflow = 0;
+  PBFS_CUDA(cudaMemcpy(&overflow, &g->ctl->overflow, sizeof(overflow), cudaMemcpyDeviceToHost),
+            "read control");
+  if (overflow) {
+    g->poisoned = true;
+    return fail(PBFS_E_CAPACITY, "dense frontier overflow");
+  }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev) {
+  if (!g || !dist_dev) return fail(PBFS_E_INPUT, "null argument");
+  *dist_dev = g->dist;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_component(pbfs_graph* g, uint64_t* n_reached, uint64_t* arcs_reached) {
+  if (!g || !n_reached || !arcs_reached) return fail(PBFS_E_INPUT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PBFS_CUDA(cudaMemsetAsync(g->comp, 0, 2 * sizeof(unsigned long long), g->stream), "memset");
+  if (g->offb == 8) {
+    component_kernel<unsigned long long><<<g->grid, kThreads, 0, g->stream>>>(
+        static_cast<const unsigned long long*>(g->rowptr), g->dist, g->n, g->comp);
+  } else {
+    component_kernel<uint32_t><<<g->grid, kThreads, 0, g->stream>>>(
+        static_cast<const uint32_t*>(g->rowptr), g->dist, g->n, g->comp);
+  }
+  PBFS_CUDA(cudaGetLastError(), "component launch");
+  unsigned long long h[2];
+  PBFS_CUDA(cudaMemcpyAsync(h, g->comp, sizeof(h), cudaMemcpyDeviceToHost, g->stream), "read");
+  PBFS_CUDA(cudaStreamSynchronize(g->stream), "component");
+  *n_reached = h[0];
+  *arcs_reached = h[1];
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(PBFS_E_INPUT, "null argument");
+  PBFS_CUDA(cudaMallocHost(out, bytes ? bytes : 16), "cudaMallocHost");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_host_free(void* p) {
+  if (p) PBFS_CUDA(cudaFreeHost(p), "cudaFreeHost");
+  return PBFS_OK;
+}
+
+}  // extern "C"
