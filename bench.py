@@ -1,0 +1,441 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 BFS hot path (BASELINE.json metric: GTEPS, harmonic
+mean over 64 seeded sources).
+
+One *step* = one traversal from each of the 64 seeded sources over the
+resident graph (one persistent-kernel launch per source), with an L2 flush
+(a 512 MiB memset, > 126 MB L2) between launches. `value` is the harmonic
+mean over sources of E_r(s) / t(s), t(s) the mean CUDA-event time of that
+source's launch over the K timed steps; E_r = (sum of reached degrees) / 2.
+
+  python bench.py [--workload rmat26] [--steps K] [--warmup W] [--gpus N]
+  python bench.py --impl reference ...   # the reference's own CPU hybrid BFS
+
+Multi-GPU (torchrun, N > 1): the 64 sources are sharded across ranks, every
+rank holding the whole graph (independent traversals, no data-path
+collective): "scaling": "weak" in sources per GPU; timing is max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (generator kind, scale/side, edge factor, device offset bytes, description)
+    "rmat20": ("kron", 20, 16, 4, "config 1: RMAT scale 20 ef16 (a,b,c,d=.57/.19/.19/.05, seed 1), "
+                                  "symmetrized, dedup, self-loops removed, int32 offsets"),
+    "er24": ("uniform", 24, 16, 8, "config 2: uniform random n=2^24, 2^28 sampled pairs (seed 1), "
+                                   "symmetrized (avg degree ~32), int64 offsets"),
+    "mesh4096": ("mesh", 4096, 0, 8, "config 3: 4096x4096 mesh, p=0.9 edges, round(0.001 n) "
+                                     "shortcuts within Manhattan 32 (seed 1), int64 offsets"),
+    "rmat26": ("kron", 26, 16, 8, "config 4: RMAT scale 26 ef16 (seed 1), symmetrized, dedup, "
+                                  "self-loops removed, int64 offsets"),
+    "rmat28": ("kron", 28, 16, 8, "config 5: RMAT scale 28 ef16 (seed 1), int64 offsets"),
+}
+METRIC = "GTEPS (harmonic mean over 64 seeded sources)"
+NUM_SOURCES = 64
+SOURCE_SEED = 1
+GRAPH_SEED = 1
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def build_graph(name: str):
+    import paper_2503_00430_b200 as pb
+    kind, s, ef, _, _ = WORKLOADS[name]
+    t0 = time.time()
+    if kind == "mesh":
+        spec = pb.GeneratorSpec(pb.GeneratorKind.Mesh, seed=GRAPH_SEED, mesh_side=s,
+                                drop_self_loops=True)
+    else:
+        spec = pb.GeneratorSpec(pb.GeneratorKind.Kronecker if kind == "kron"
+                                else pb.GeneratorKind.UniformRandom, s, ef, GRAPH_SEED,
+                                drop_self_loops=True)
+    g = pb.generate(spec)
+    log(f"[bench] generated {name}: n={g.vertex_count} m={g.edge_count} in {time.time()-t0:.1f}s")
+    return g
+
+
+def kernel_config(graph):
+    import paper_2503_00430_b200 as pb
+    stats = pb.compute_stats(graph)
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid)
+    # run_bfs's category dispatcher (kernels.cpp:657-662)
+    if stats.category == pb.GraphCategory.LargeDiameter:
+        cfg.force_top_down_only = True
+    return cfg, stats
+
+
+def choose_sources(graph, dg, cfg, workload):
+    """pick_sources (bfsbench.cpp:206-235, seed 1); for the mesh also keep only
+    sources inside the largest component."""
+    import paper_2503_00430_b200 as pb
+    if workload != "mesh4096":
+        return pb.pick_sources(graph, NUM_SOURCES, SOURCE_SEED)
+    cand = pb.pick_sources(graph, 4 * NUM_SOURCES, SOURCE_SEED)
+    for c in cand:
+        res = dg.bfs(int(c), cfg, want_trace=False)
+        reached = res.distances != 0xFFFFFFFF
+        if reached.sum() * 2 > graph.vertex_count:
+            keep = [int(v) for v in cand if reached[v]]
+            return np.array(keep[:NUM_SOURCES], dtype=np.uint32)
+    raise RuntimeError("no giant component found")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7 and parts[0].isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(int(r[0]) for r in rows),
+                "sm_max_mhz": max(int(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def harmonic(values):
+    values = [v for v in values if v > 0]
+    return len(values) / sum(1.0 / v for v in values) if values else 0.0
+
+
+def cpu_reference_run(graph, sources, cfg, budget_s: float, e_r: dict, check_dist=None):
+    """The reference's own hybrid BFS (oracle/_ref, all host threads) on the
+    same CSR and sources; returns (per-source GTEPS list, sample text, cores,
+    kind, mismatches)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    kind = "reference"
+    try:
+        ref = oracle.ref()
+    except Exception as exc:  # the reference library did not travel: port
+        log(f"[bench] reference library unavailable ({exc}); timing the oracle port")
+        ref = None
+    gteps, done, mismatches = [], 0, 0
+    t_start = time.time()
+    if ref is not None:
+        rg = ref.from_csr(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
+                          graph.symmetric)
+        for s in sources:
+            dist, _, wall_ns = ref.run(rg, int(s), 3, workers=threads,
+                                       force_td=cfg.force_top_down_only,
+                                       want_dist=check_dist is not None)
+            if check_dist is not None and int(s) in check_dist:
+                mismatches += int(not np.array_equal(dist, check_dist[int(s)]))
+            gteps.append(e_r[int(s)] / (wall_ns * 1e-9) / 1e9)
+            done += 1
+            if time.time() - t_start > budget_s:
+                break
+        sample = (f"{done} of {len(sources)} sources, 1 run each, parbfs::bfs_hybrid "
+                  f"(threshold 0.05{', force_top_down_only' if cfg.force_top_down_only else ''}) "
+                  f"with worker_count={threads}, steady-clock wall per call incl. its setup")
+    else:
+        kind, threads = "port", 1
+        port = oracle.port()
+        for s in sources:
+            t0 = time.perf_counter_ns()
+            port.bfs_serial(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
+                            int(s))
+            gteps.append(e_r[int(s)] / ((time.perf_counter_ns() - t0) * 1e-9) / 1e9)
+            done += 1
+            if time.time() - t_start > budget_s:
+                break
+        sample = f"{done} of {len(sources)} sources, oracle serial BFS, 1 thread"
+    return gteps, sample, threads, kind, mismatches
+
+
+def run_reference_arm(args):
+    """bench.py --impl reference: rank 0 only, the reference CPU BFS."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2503_00430_b200 as pb
+    graph = build_graph(args.workload)
+    cfg, _ = kernel_config(graph)
+    sources = pb.pick_sources(graph, NUM_SOURCES, SOURCE_SEED)
+    deg = graph.degrees()
+    # E_r per source from the reference's own serial traversal would cost
+    # minutes at scale 26; the reference hybrid returns distances, so E_r is
+    # taken from each run's reached set.
+    import oracle
+    ref = oracle.ref()
+    rg = ref.from_csr(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
+                      graph.symmetric)
+    threads = os.cpu_count() or 1
+    per_step = []
+    all_gteps = []
+    budget = args.ref_step_budget
+    for step in range(args.warmup + args.steps):
+        t_step = time.time()
+        g_list = []
+        for s in sources:
+            dist, _, wall_ns = ref.run(rg, int(s), 3, workers=threads,
+                                       force_td=cfg.force_top_down_only)
+            e_r = float(deg[dist != 0xFFFFFFFF].sum()) / 2.0
+            g_list.append(e_r / (wall_ns * 1e-9) / 1e9)
+            if time.time() - t_step > budget:
+                break
+        if step >= args.warmup:
+            per_step.append(time.time() - t_step)
+            all_gteps.extend(g_list)
+    value = harmonic(all_gteps)
+    sample = (f"{len(all_gteps)} source runs over {args.steps} steps (each step <= "
+              f"{budget:.0f}s of the 64 sources), parbfs::bfs_hybrid worker_count={threads}")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GTEPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.mean(per_step), 3) if per_step else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args, graph),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GTEPS", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args, graph):
+    kind, s, ef, offb, desc = WORKLOADS[args.workload]
+    return {"workload": args.workload, "description": desc, "vertices": graph.vertex_count,
+            "directed_arcs": graph.edge_count, "offset_bytes": offb, "sources": NUM_SOURCES,
+            "source_seed": SOURCE_SEED, "graph_seed": GRAPH_SEED, "variant": "hybrid",
+            "l2": "flushed (512 MiB memset) between launches",
+            "parallelism": f"sources sharded over {args.gpus} GPU(s), graph replicated"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="rmat26", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0,
+                    help="seconds of reference CPU work for cpu_baseline")
+    ap.add_argument("--ref-step-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import paper_2503_00430_b200 as pb
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    graph = build_graph(args.workload)
+    cfg, stats = kernel_config(graph)
+    offb = WORKLOADS[args.workload][3]
+    t0 = time.time()
+    dg = graph.device(local, offb)
+    upload_s = time.time() - t0
+    log(f"[bench] resident on cuda:{local} in {upload_s:.1f}s, grid={dg.info['grid_blocks']}x"
+        f"{dg.info['block_threads']}, {dg.info['device_bytes']/2**30:.2f} GiB")
+
+    all_sources = choose_sources(graph, dg, cfg, args.workload)
+    sources = [int(s) for s in all_sources[rank::world]]
+    # A dedicated (non-default) stream: the kernel, the L2 flush and the
+    # timing events must all be ordered on the same stream.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    assert sptr != 0
+    n = graph.vertex_count
+    w_off = offb
+
+    # Untimed pass: per-source E_r and algorithmic bytes.
+    e_r, b_alg = {}, {}
+    for s in sources:
+        dg.bfs_async(s, cfg, sptr)
+        dg.sync(sptr)
+        nr, ar = dg.component()
+        e_r[s] = ar / 2.0
+        b_alg[s] = 4.0 * ar + 2.0 * w_off * nr + 4.0 * n
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    ev = {s: [] for s in sources}
+
+    def step(timed: bool):
+        pairs = []
+        for s in sources:
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dg.bfs_async(s, cfg, sptr)
+            b.record(stream)
+            pairs.append((s, a, b))
+        return pairs
+
+    for _ in range(args.warmup):
+        step(False)
+    dg.sync(sptr)
+    torch.cuda.synchronize()
+    if dist_on:
+        tdist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        recorded = []
+        for _ in range(args.steps):
+            recorded.extend(step(True))
+            launches += len(sources)
+        end.record(stream)
+        dg.sync(sptr)
+        torch.cuda.synchronize()
+    clk = clocks.summary()
+    total_ms = start.elapsed_time(end)
+    for s, a, b in recorded:
+        ev[s].append(a.elapsed_time(b))
+    t_src = {s: statistics.mean(ev[s]) for s in sources}  # ms
+
+    # max over ranks of the step time; gather per-source figures
+    ms_per_step = total_ms / args.steps
+    local_rows = [(s, e_r[s], b_alg[s], t_src[s]) for s in sources]
+    if dist_on:
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, (ms_per_step, local_rows))
+        ms_per_step = max(x[0] for x in gathered)
+        rows = [r for x in gathered for r in x[1]]
+    else:
+        rows = local_rows
+    gteps = [er / (t * 1e-3) / 1e9 for _, er, _, t in rows]
+    value = harmonic(gteps)
+    achieved = sum(b for _, _, b, _ in rows) / sum(t * 1e-3 for _, _, _, t in rows) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # e2e: the public API call with host buffers (pinned), D2H of the
+    # distance array inside the timed region, one pass over this rank's sources.
+    host = pb.parbfs.pinned_empty(n, np.uint32)
+    e2e_rows = []
+    for s in sources:
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = dg.bfs(s, cfg, want_trace=False, out=host)
+        t1 = time.perf_counter()
+        e2e_rows.append(e_r[s] / (t1 - t0) / 1e9)
+    if dist_on:
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, e2e_rows)
+        e2e_rows = [x for g_ in gathered for x in g_]
+    e2e_value = harmonic(e2e_rows)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        check = {}
+        for s in sources[:2]:
+            check[s] = dg.bfs(s, cfg, want_trace=False).distances.copy()
+        cg, sample, cores, kind, mism = cpu_reference_run(graph, sources, cfg, args.cpu_budget,
+                                                          e_r, check)
+        cpu = {"value": round(harmonic(cg), 4), "unit": "GTEPS", "cores": cores, "kind": kind,
+               "sample": sample, "parity_checked_sources": len(check),
+               "parity_mismatches": mism}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {**workload_config(args, graph),
+                                            "graph_upload_s": round(upload_s, 2),
+                                            "mean_bfs_ms": round(statistics.mean(
+                                                t for *_, t in rows), 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "bfs_persistent (one cooperative launch per BFS)",
+                         "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4 * NUM_SOURCES,
+                    "d2h_bytes_per_step": 4 * n * NUM_SOURCES,
+                    "note": "pbfs_bfs C-ABI call per source, distances copied to a host buffer"},
+            "gpu_launches": launches * world,
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    if dist_on:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -527,6 +528,17 @@ class DeviceGraph:
         ar = ctypes.c_uint64()
         _check(lib.pbfs_graph_component(self.h, ctypes.byref(nr), ctypes.byref(ar)))
         return nr.value, ar.value
+
+
+def pinned_empty(count: int, dtype=np.uint32) -> np.ndarray:
+    """A page-locked host array (cudaMallocHost) for full-bandwidth D2H copies."""
+    dtype = np.dtype(dtype)
+    nbytes = max(int(count) * dtype.itemsize, 1)
+    p = ctypes.c_void_p()
+    _check(lib.pbfs_host_alloc(nbytes, ctypes.byref(p)))
+    buf = (ctypes.c_uint8 * nbytes).from_address(p.value)
+    weakref.finalize(buf, lib.pbfs_host_free, ctypes.c_void_p(p.value))
+    return np.frombuffer(buf, dtype=dtype, count=int(count))
 
 
 def _gpu_run(graph: CsrGraph, source: int, config: KernelConfig, variant: KernelVariant,
