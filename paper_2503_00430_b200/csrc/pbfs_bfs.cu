@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -48,6 +49,8 @@ struct pbfs_graph {
   uint32_t rec_cap = 0;
   uint64_t qcap = 0, heavy_cap = 0;
   int grid = 0;
+  size_t bitmap_bytes = 0;
+  size_t persist_bytes = 0;  // L2 set-aside granted for the bitmap window
   uint64_t device_bytes = 0;
   std::vector<void*> allocs;
   bool poisoned = false;  // a launch failed; ctl must be reset
@@ -159,9 +162,28 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.threshold = cfg->hybrid_threshold_fraction;
   p.alpha = cfg->alpha;
   p.beta = cfg->beta;
-  void* args[] = {&p};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&bfs_persistent<C, OffT>),
-                                     dim3(g->grid), dim3(kThreads), args, 0, s);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(g->grid);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  int nattr = 1;
+  if (g->persist_bytes) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = g->visited;
+    attr[1].val.accessPolicyWindow.num_bytes = g->bitmap_bytes;
+    attr[1].val.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(g->persist_bytes) / static_cast<float>(g->bitmap_bytes));
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nattr = 2;
+  }
+  lc.attrs = attr;
+  lc.numAttrs = nattr;
+  return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT>, p);
 }
 
 cudaError_t launch(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, const Launch& l,
@@ -336,12 +358,17 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
 
   const size_t wbytes = static_cast<size_t>(g->words) * 4;
   if ((st = dalloc(g, &g->rowptr, (n + 1) * offb)) != PBFS_OK) return bail(st);
-  if ((st = dalloc(g, &g->col, m * 4)) != PBFS_OK) return bail(st);
+  // Padded to whole 16 B vectors: hub chunks are read with uint4 loads.
+  if ((st = dalloc(g, &g->col, ((m + 3) / 4) * 16 + 16)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->init_mask, wbytes)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->dist, ((n + 3) / 4) * 16)) != PBFS_OK) return bail(st);
-  if ((st = dalloc(g, &g->visited, wbytes)) != PBFS_OK) return bail(st);
-  if ((st = dalloc(g, &g->bm[0], wbytes)) != PBFS_OK) return bail(st);
-  if ((st = dalloc(g, &g->bm[1], wbytes)) != PBFS_OK) return bail(st);
+  // visited | frontier | next bitmaps in one block: the probe-heavy working
+  // set (3 n/8 bytes) sits under one persisting L2 access-policy window so
+  // the multi-GB `col` stream cannot evict it.
+  if ((st = dalloc(g, &g->visited, 3 * wbytes)) != PBFS_OK) return bail(st);
+  g->bm[0] = g->visited + g->words;
+  g->bm[1] = g->visited + 2 * static_cast<size_t>(g->words);
+  g->bitmap_bytes = 3 * wbytes;
   if ((st = dalloc(g, &g->queue[0], g->qcap * 4)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->queue[1], g->qcap * 4)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->heavy, std::max<uint64_t>(g->heavy_cap, 1) * sizeof(HeavyItem))) != PBFS_OK)
@@ -383,6 +410,21 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   }
   if (occ < 1) return bail(fail(PBFS_E_DEVICE, "traversal kernel cannot be resident"));
   g->grid = prop.multiProcessorCount * occ;
+  // Persisting L2 set-aside for the bitmap block (process-wide device limit;
+  // only ever raised). PBFS_NO_L2_PERSIST=1 disables it for A/B runs.
+  const char* no_persist = std::getenv("PBFS_NO_L2_PERSIST");
+  if (prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0 &&
+      !(no_persist && no_persist[0] == '1')) {
+    g->bitmap_bytes = std::min<size_t>(g->bitmap_bytes, prop.accessPolicyMaxWindowSize);
+    const size_t want = std::min<size_t>(g->bitmap_bytes, prop.persistingL2CacheMaxSize);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+      cudaGetLastError();
+    } else {
+      g->persist_bytes = want;
+    }
+  }
   cudaSetDevice(prev);
   *out = g;
   return PBFS_OK;

@@ -39,9 +39,9 @@ namespace dev {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kHeavyDeg = 256;  // degree above which a vertex is split
-constexpr uint32_t kChunk = 1024;    // edges per heavy work item
-constexpr int kPushBuf = 256;        // per-warp discovery buffer (entries)
+constexpr uint32_t kHeavyDeg = 1024; // degree above which a vertex is split
+constexpr uint32_t kChunk = 2048;    // edges per heavy work item
+constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
@@ -128,6 +128,31 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Predicated claim atomics: one SASS instruction under a predicate instead of
+// a divergent branch per edge slot. `old` keeps its input when not executed.
+__device__ __forceinline__ uint32_t atom_or_if(bool pred, uint32_t* addr, uint32_t val,
+                                               uint32_t old) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q atom.global.or.b32 %0, [%1], %3;\n\t}"
+      : "+r"(old)
+      : "l"(addr), "r"((uint32_t)pred), "r"(val));
+  return old;
+}
+__device__ __forceinline__ uint32_t atom_cas_if(bool pred, uint32_t* addr, uint32_t cmp,
+                                                uint32_t val, uint32_t old) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q atom.global.cas.b32 %0, [%1], %3, %4;\n\t}"
+      : "+r"(old)
+      : "l"(addr), "r"((uint32_t)pred), "r"(cmp), "r"(val));
+  return old;
+}
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -147,7 +172,9 @@ struct GridBarrier {
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(&ctl->bar_count, 1ull);
-      while (ld_acquire(&ctl->bar_count) < target) __nanosleep(32);
+      // Relaxed polling: an acquire load per spin would invalidate this SM's
+      // L1 on every iteration (CCTL.IVALL) under the other resident CTAs.
+      while (ld_relaxed64(&ctl->bar_count) < target) __nanosleep(32);
       __threadfence();
     }
     __syncthreads();
@@ -174,6 +201,31 @@ struct WarpPush {
     count = 0;
     __syncwarp();
   }
+  // Appends lane-local winners v[k] (bit k of winmask) of a K-slot batch with
+  // one warp scan and at most one flush.
+  template <int K>
+  __device__ __forceinline__ void push_many(uint32_t winmask, const uint32_t (&v)[K],
+                                            uint32_t* out, unsigned long long* counter,
+                                            unsigned long long cap, unsigned int* overflow) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lane = lane_id();
+    const uint32_t c = __popc(winmask);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (unsigned)o) incl += x;
+    }
+    const int total = (int)__shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    if (count + total > kPushBuf) flush(out, counter, cap, overflow);
+    uint32_t pos = count + incl - c;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if ((winmask >> k) & 1u) buf[pos++] = v[k];
+    }
+    count += total;
+  }
   __device__ __forceinline__ void push(bool want, uint32_t v, uint32_t* out,
                                        unsigned long long* counter, unsigned long long cap,
                                        unsigned int* overflow) {
@@ -186,63 +238,106 @@ struct WarpPush {
   }
 };
 
-// Edge (u -> v) at depth d: the claim discipline of the variant. Returns
-// whether v is appended to the next queue; *distinct says whether this
-// append is the vertex's first discovery.
-template <int C, typename OffT>
-__device__ __forceinline__ bool visit(const Params<OffT>& p, uint32_t v, uint32_t nd,
-                                      bool& distinct, unsigned long long& viol) {
-  const uint32_t w = v >> 5, bit = 1u << (v & 31);
-  if constexpr (C == kClaimCas) {
-    // kernels.cpp:282-290: claim by compare-exchange from kUnreached.
-    if (ld_relaxed(&p.dist[v]) == kUnreached &&
-        atomicCAS(&p.dist[v], kUnreached, nd) == kUnreached) {
-      distinct = true;
-      return true;
-    }
-    return false;
-  } else if constexpr (C == kClaimPlain) {
-    // kernels.cpp:291-301: load, compare, plain store; racing writers all
-    // store the same nd, so duplicates are possible but values are not.
-    const uint32_t cur = ld_relaxed(&p.dist[v]);
-    if (nd < cur) {
-      if (p.validate && cur != kUnreached) ++viol;  // kernels.cpp:294
-      p.dist[v] = nd;
-      // The visited bitmap is only a distinct-count ledger here.
-      const uint32_t old = atomicOr(&p.visited[w], bit);
-      distinct = !(old & bit);
-      return true;
-    }
-    return false;
-  } else {
-    // kernels.cpp:302-320: test the visited bit, claim it, store dist inline.
-    if (!(ld_relaxed(&p.visited[w]) & bit)) {
-      const uint32_t old = atomicOr(&p.visited[w], bit);
-      if (!(old & bit)) {
-        p.dist[v] = nd;
-        distinct = true;
-        return true;
-      }
-    }
-    return false;
-  }
-}
-
 template <typename OffT>
 __device__ __forceinline__ unsigned long long degree_of(const Params<OffT>& p, uint32_t v) {
-  return (unsigned long long)(p.rowptr[v + 1] - p.rowptr[v]);
+  return (unsigned long long)(__ldg(&p.rowptr[v + 1]) - __ldg(&p.rowptr[v]));
 }
 
 struct WarpTally {
   unsigned long long produced = 0, raw = 0, edges = 0, degree = 0, viol = 0;
 };
 
-// One warp-cooperative step over up to 32 edges: lane processes edge e of the
-// batch (owner found by a shuffle binary search over inclusive degree sums).
+// Probe word for the claim test, read at L2 (ld.global.cg): an L1 copy would
+// never see other SMs' claims made during the level, so every edge into a
+// not-yet-claimed vertex would go on to issue an L2 atomic. At L2 the probe
+// sees a claim as soon as it lands, which keeps atomics close to one per
+// discovered vertex.
+template <int C, typename OffT>
+__device__ __forceinline__ uint32_t probe_word(const Params<OffT>& p, uint32_t v) {
+  if constexpr (C == kClaimBitmap) {
+    return __ldcg(&p.visited[v >> 5]);
+  } else {
+    return __ldcg(&p.dist[v]);
+  }
+}
+
+// The claim discipline of each variant for K edges (u -> v[k]) of one lane,
+// in three stages so nothing waits on a single round trip: all K probe
+// loads, then all K claim atomics (results consumed only afterwards), then
+// the dist stores and queue appends. okm bit k marks a live edge slot.
+template <int C, int K, typename OffT>
+__device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
+                                            const uint32_t (&v)[K], uint32_t okm,
+                                            uint32_t* qout, WarpPush& wp, LevelCnt* cnt,
+                                            WarpTally& t) {
+  // Unconditional probes (dead slots hold a valid vertex id): predicated
+  // loads end up in separate blocks that ptxas interleaves with their uses,
+  // serialising the round trips this batching exists to overlap.
+  uint32_t w[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) w[k] = probe_word<C>(p, v[k]);
+  if constexpr (C == kClaimPlain) {
+    // kernels.cpp:291-301: compare, plain store; racing writers all store the
+    // same nd, so duplicates are possible but values are not. Every racing
+    // writer also ORs the same bit into the next-frontier bitmap (no-return
+    // RED, idempotent like the reference's same-value byte stores):
+    // duplicates are counted (raw) but collapse in the bitmap, which is
+    // compacted into the next queue after the level.
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (((okm >> k) & 1u) && nd < w[k]) {
+        if (p.validate && w[k] != kUnreached) ++t.viol;  // kernels.cpp:294
+        p.dist[v[k]] = nd;
+        ++t.raw;
+        atomicOr(&p.bm[1][v[k] >> 5], 1u << (v[k] & 31));
+      }
+    }
+    (void)qout;
+    (void)wp;
+    (void)cnt;
+  } else {
+    // Stage 2: predicated claim atomics, all issued before any result is used.
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool live = (okm >> k) & 1u;
+      if constexpr (C == kClaimCas) {
+        // kernels.cpp:282-290: claim by compare-exchange from kUnreached.
+        w[k] = atom_cas_if(live && w[k] == kUnreached, &p.dist[v[k]], kUnreached, nd, 0u);
+      } else {
+        // kernels.cpp:302-320: test the visited bit, then claim it.
+        const uint32_t bit = 1u << (v[k] & 31);
+        w[k] = atom_or_if(live && !(w[k] & bit), &p.visited[v[k] >> 5], bit, 0xffffffffu);
+      }
+    }
+    // Stage 3: winners store dist inline (plain store) and are appended.
+    uint32_t winmask = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool won = C == kClaimCas ? w[k] == kUnreached : !(w[k] & (1u << (v[k] & 31)));
+      winmask |= (uint32_t)won << k;
+      if constexpr (C == kClaimBitmap) {
+        if (won) p.dist[v[k]] = nd;
+      }
+    }
+    t.produced += __popc(winmask);
+    if (p.policy == kPolicyBeamer) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if ((winmask >> k) & 1u) t.degree += degree_of(p, v[k]);
+      }
+    }
+    wp.push_many<K>(winmask, v, qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  }
+}
+
+// Warp-cooperative expansion of up to 32 light vertices (lane i holds vertex
+// i's [beg, beg+deg)): inclusive shuffle scan of the degrees, then 4x32 edges
+// per step, each lane locating its owner by a 5-step shuffle binary search.
 template <int C, typename OffT>
 __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t nd, OffT beg,
                                                uint32_t deg, uint32_t* qout, WarpPush& wp,
                                                LevelCnt* cnt, WarpTally& t) {
+  constexpr int K = 16;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   uint32_t incl = deg;
@@ -253,31 +348,36 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
   }
   const uint32_t total = __shfl_sync(FULL, incl, 31);
   const uint32_t excl = incl - deg;
-  for (uint32_t e0 = 0; e0 < total; e0 += 32) {
-    const uint32_t e = e0 + lane;
-    int j = 0;
+  if (total == 0) return;
+  // First edge of the batch: owner = first lane with a non-empty range.
+  const unsigned nz = __ballot_sync(FULL, deg != 0);
+  const OffT b0 = __shfl_sync(FULL, beg, __ffs(nz) - 1);
+  for (uint32_t e0 = 0; e0 < total; e0 += 32 * K) {
+    uint32_t v[K];
+    uint32_t okm = 0;
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const uint32_t x = __shfl_sync(FULL, incl, j + step - 1);
-      if (x <= e) j += step;
+    for (int k = 0; k < K; ++k) {
+      const uint32_t e = e0 + 32 * k + lane;
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t x = __shfl_sync(FULL, incl, j + step - 1);
+        if (x <= e) j += step;
+      }
+      const OffT ob = __shfl_sync(FULL, beg, j);
+      const uint32_t oex = __shfl_sync(FULL, excl, j);
+      const bool ok = e < total;
+      okm |= (uint32_t)ok << k;
+      // Dead slots re-read the batch's first edge (always valid): no branch.
+      const unsigned long long ei = ok ? (unsigned long long)ob + (e - oex) : (unsigned long long)b0;
+      v[k] = __ldcs(&p.col[ei]);
     }
-    const OffT ob = __shfl_sync(FULL, beg, j);
-    const uint32_t oex = __shfl_sync(FULL, excl, j);
-    bool want = false, distinct = false;
-    uint32_t v = 0;
-    if (e < total) {
-      v = __ldg(&p.col[ob + (e - oex)]);
-      want = visit<C>(p, v, nd, distinct, t.viol);
-    }
-    if (distinct) {
-      ++t.produced;
-      if (p.policy == kPolicyBeamer) t.degree += degree_of(p, v);
-    }
-    t.raw += want;
-    wp.push(want, v, qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t);
   }
 }
 
+// Static-first work distribution: warp gw takes slice gw first and only
+// then falls back to an atomic cursor, so a tiny frontier costs no atomics.
 template <int C, typename OffT>
 __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint32_t* qin,
                                unsigned long long qlen, uint32_t* qout, WarpPush& wp,
@@ -285,12 +385,10 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
-  for (;;) {
-    unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(&cnt->td_cursor, 32u);
-    base = __shfl_sync(FULL, base, 0);
-    if (base >= qlen) break;
-    const unsigned long long i = (unsigned long long)base + lane;
+  const unsigned warps_total = gridDim.x * kWarps;
+  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
+  while (base < qlen) {
+    const unsigned long long i = base + lane;
     OffT beg = 0, end = 0;
     if (i < qlen) {
       const uint32_t u = qin[i];
@@ -299,67 +397,90 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
     }
     unsigned long long deg = (unsigned long long)(end - beg);
     t.edges += deg;
-    if (deg > kHeavyDeg) {
-      // Hub: split into kChunk-edge items for the grid-wide heavy pass.
-      const unsigned int items = (unsigned int)((deg + kChunk - 1) / kChunk);
-      const unsigned int slot = atomicAdd(&cnt->heavy_count, items);
-      if ((unsigned long long)slot + items <= p.heavy_cap) {
-        for (unsigned int k = 0; k < items; ++k) {
+    // Hubs: split into kChunk-edge items for the grid-wide heavy pass; the
+    // warp reserves all its items with one atomicAdd (a per-vertex atomic on
+    // one counter serialises at L2 when a level holds ~1e6 hubs).
+    const bool hub = deg > kHeavyDeg;
+    const unsigned int my_items = hub ? (unsigned int)((deg + kChunk - 1) / kChunk) : 0u;
+    if (__any_sync(FULL, hub)) {
+      unsigned int incl = my_items;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (unsigned)o) incl += x;
+      }
+      const unsigned int wtotal = __shfl_sync(FULL, incl, 31);
+      unsigned int wbase = 0;
+      if (lane == 0) wbase = atomicAdd(&cnt->heavy_count, wtotal);
+      wbase = __shfl_sync(FULL, wbase, 0);
+      if ((unsigned long long)wbase + wtotal <= p.heavy_cap) {
+        const unsigned int slot = wbase + incl - my_items;
+        for (unsigned int k = 0; k < my_items; ++k) {
           const unsigned long long b = (unsigned long long)beg + (unsigned long long)k * kChunk;
           const unsigned long long e = b + kChunk < (unsigned long long)end ? b + kChunk
                                                                             : (unsigned long long)end;
           p.heavy[slot + k] = HeavyItem{b, e};
         }
-      } else {
+      } else if (lane == 0) {
         atomicExch(&p.ctl->overflow, 1u);
       }
-      deg = 0;
     }
+    if (hub) deg = 0;
     td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t);
+    unsigned int nb = 0;
+    if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
+    base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
   }
 }
 
+// Hub chunks: 16 coalesced 128 B `col` loads per warp step, laid out so the
+// 32 lanes of every load (and hence of every visited-bitmap probe and claim
+// that follows) hold 32 CONSECUTIVE neighbours of the sorted adjacency list.
+// A hub's neighbours are dense in id space, so one probe instruction touches
+// ~2-3 distinct 128 B bitmap lines instead of ~32 -- the L1TEX line rate, not
+// DRAM, is what bounds a random-probe loop on this part.
 template <int C, typename OffT>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
                                uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t) {
+  constexpr int K = 16;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
-  for (;;) {
-    unsigned int it = 0;
-    if (lane == 0) it = atomicAdd(&cnt->heavy_cursor, 1u);
-    it = __shfl_sync(FULL, it, 0);
-    if (it >= items) break;
+  const unsigned warps_total = gridDim.x * kWarps;
+  unsigned int it = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  while (it < items) {
     const HeavyItem h = p.heavy[it];
-    for (unsigned long long e0 = h.beg; e0 < h.end; e0 += 128) {
-      // Four independent coalesced loads in flight per lane.
-      uint32_t v[4];
-      bool ok[4];
+    const uint32_t* base = p.col + h.beg;
+    const uint32_t len = (uint32_t)(h.end - h.beg);
+    for (uint32_t e0 = 0; e0 < len; e0 += 32 * K) {
+      uint32_t v[K];
+      uint32_t okm = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const unsigned long long e = e0 + k * 32 + lane;
-        ok[k] = e < h.end;
-        v[k] = ok[k] ? __ldg(&p.col[e]) : 0;
+      for (int k = 0; k < K; ++k) {
+        const uint32_t e = e0 + 32 * k + lane;
+        const bool ok = e < len;
+        okm |= (uint32_t)ok << k;
+        v[k] = __ldcs(&base[ok ? e : 0u]);
       }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bool distinct = false;
-        const bool want = ok[k] && visit<C>(p, v[k], nd, distinct, t.viol);
-        if (distinct) {
-          ++t.produced;
-          if (p.policy == kPolicyBeamer) t.degree += degree_of(p, v[k]);
-        }
-        t.raw += want;
-        wp.push(want, v[k], qout, &cnt->raw, p.qcap, &p.ctl->overflow);
-      }
+      claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t);
     }
+    // Items are equal-sized (kChunk edges but a hub's last one): a static
+    // round-robin balances them without a contended cursor.
+    it += warps_total;
   }
+  (void)FULL;
+  (void)cnt;
 }
 
-// Bottom-up over all vertices (kernels.cpp:340-382).
+// Bottom-up over all vertices (kernels.cpp:340-382). Each lane carries KB
+// unvisited vertices at once: the offsets, first neighbours and their
+// frontier words of all KB are loaded before any is resolved; most vertices
+// find a parent at the first probe (RMAT hubs sort first), the rest continue
+// with a serial early-exit scan.
 template <typename OffT>
 __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
                          uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t) {
+  constexpr int KB = 2;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
@@ -394,22 +515,43 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
     }
     if (owner) found[lane] = 0;
     __syncwarp();
-    for (uint32_t k = 0; k < total; k += 32) {
-      const uint32_t idx = k + lane;
-      if (idx < total) {
-        const uint32_t v = list[idx];
-        const OffT beg = __ldg(&p.rowptr[v]);
-        const OffT end = __ldg(&p.rowptr[v + 1]);
-        for (OffT e = beg; e < end; ++e) {
-          const uint32_t u = __ldg(&p.col[e]);
-          ++t.edges;
-          if ((front[u >> 5] >> (u & 31)) & 1u) {
-            p.dist[v] = nd;
-            atomicOr(&found[(v >> 5) - g * kGroupWords], 1u << (v & 31));
-            ++t.produced;
-            if (p.policy == kPolicyBeamer) t.degree += (unsigned long long)(end - beg);
-            break;
-          }
+    for (uint32_t k = 0; k < total; k += 32 * KB) {
+      uint32_t v[KB], u[KB], fw[KB];
+      OffT beg[KB], end[KB];
+      bool valid[KB];
+      // Branch-free loads (dead slots read vertex list[0]'s data; `col` is
+      // padded so col[m] is readable) so ptxas keeps them overlapped.
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        const uint32_t idx = k + 32 * q + lane;
+        valid[q] = idx < total;
+        v[q] = list[valid[q] ? idx : 0];
+        beg[q] = __ldg(&p.rowptr[v[q]]);
+        end[q] = __ldg(&p.rowptr[v[q] + 1]);
+      }
+#pragma unroll
+      for (int q = 0; q < KB; ++q) u[q] = __ldcs(&p.col[beg[q]]);
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        fw[q] = front[u[q] >> 5];
+        if (!valid[q]) end[q] = beg[q];
+      }
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        if (beg[q] >= end[q]) continue;
+        bool hit = (fw[q] >> (u[q] & 31)) & 1u;
+        unsigned long long scanned = 1;
+        for (OffT e = beg[q] + 1; !hit && e < end[q]; ++e) {
+          const uint32_t x = __ldg(&p.col[e]);
+          ++scanned;
+          hit = (front[x >> 5] >> (x & 31)) & 1u;
+        }
+        t.edges += scanned;
+        if (hit) {
+          p.dist[v[q]] = nd;
+          atomicOr(&found[(v[q] >> 5) - g * kGroupWords], 1u << (v[q] & 31));
+          ++t.produced;
+          if (p.policy == kPolicyBeamer) t.degree += (unsigned long long)(end[q] - beg[q]);
         }
       }
     }
@@ -435,12 +577,46 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
   }
   if (lane_id() == 0) {
     if (t.produced) atomicAdd(&cnt->produced, t.produced);
+    if (add_raw && t.raw) atomicAdd(&cnt->raw, t.raw);
     if (t.edges) atomicAdd(&cnt->edges, t.edges);
     if (t.degree) atomicAdd(&cnt->degree, t.degree);
     if (t.viol) atomicAdd(&cnt->violations, t.viol);
-    (void)add_raw;
   }
   t = WarpTally{};
+}
+
+// Bitmap -> queue (count_bitmap_slice / write_dense_slice, kernels.cpp:
+// 225-241): each warp compacts 32 words with a popcount scan and reserves its
+// output range with one atomicAdd; optionally clears the words it consumed.
+__device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
+                                               unsigned int* counter, bool clear) {
+  const unsigned lane = lane_id();
+  const unsigned warps_total = gridDim.x * kWarps;
+  const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  for (uint32_t base = gw * 32; base < words; base += warps_total * 32) {
+    const uint32_t w = base + lane;
+    const uint32_t word = w < words ? nb[w] : 0u;
+    if (clear && word) nb[w] = 0;
+    const uint32_t c = __popc(word);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += x;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) continue;
+    unsigned int off = 0;
+    if (lane == 0) off = atomicAdd(counter, total);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    uint32_t pos = off + incl - c;
+    uint32_t bits = word;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      q[pos++] = w * 32 + b;
+    }
+  }
 }
 
 template <int C, typename OffT>
@@ -471,6 +647,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
       const uint32_t sb = (w == (src >> 5)) ? (1u << (src & 31)) : 0u;
       p.visited[w] = p.init_mask[w] | sb;
       p.bm[0][w] = sb;
+      p.bm[1][w] = 0;
     }
     if (leader) {
       p.queue[0][0] = src;
@@ -513,23 +690,35 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
       ctl->cnt[(depth + 2) & 3] = z;
     }
     WarpTally t;
+    unsigned long long dbg_mid = 0, dbg_items = 0;
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
       td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t);
       if (p.max_degree > kHeavyDeg) {
         bar.sync();
         const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
+        if (leader) {
+          dbg_mid = globaltimer();
+          dbg_items = items;
+        }
         if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
       bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t);
     }
-    warp_flush_tally(cnt, t, false);
+    warp_flush_tally(cnt, t, C == kClaimPlain);
     bar.sync();
+    if constexpr (C == kClaimPlain) {
+      // BFS-NonAtomic: the marks collapse into the distinct next frontier.
+      compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true);
+      bar.sync();
+    }
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
-    const unsigned long long produced = *(volatile unsigned long long*)&cnt->produced;
+    const unsigned long long produced =
+        C == kClaimPlain ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
+                         : *(volatile unsigned long long*)&cnt->produced;
     const unsigned long long raw = td ? *(volatile unsigned long long*)&cnt->raw : produced;
     const unsigned long long edges = *(volatile unsigned long long*)&cnt->edges;
     const unsigned long long pdeg = *(volatile unsigned long long*)&cnt->degree;
@@ -544,7 +733,8 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
         r.distinct_size = cur_distinct;
         r.duplicate_count = cur_raw - cur_distinct;
         r.edges_examined = edges;
-        r.flush_events = 0;
+        // DIAGNOSTIC (temporary): heavy items << 32 | light-phase microseconds
+        r.flush_events = dbg_mid ? (dbg_items << 32) | ((dbg_mid - t_start) / 1000) : 0;
         r.elapsed_ns = (long long)(now - t_start);
         p.records[depth] = r;
       }
@@ -560,7 +750,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
     const bool next_td = decide(td, produced, pdeg, consumed, unvisited_edges);
     if (td && next_td) {
       qcur ^= 1;
-      qlen = raw;
+      qlen = C == kClaimPlain ? produced : raw;
     } else if (!td && !next_td) {
       fcur ^= 1;
     } else if (td && !next_td) {
@@ -578,33 +768,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
     } else {
       // Entering top-down: ascending queue from the produced bitmap
       // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241).
-      const uint32_t* nb = p.bm[fcur ^ 1];
-      uint32_t* q = p.queue[qcur];
-      const unsigned warps_total = gridDim.x * kWarps;
-      const unsigned gw = blockIdx.x * kWarps + warp;
-      for (uint32_t base = gw * 32; base < p.words; base += warps_total * 32) {
-        const uint32_t w = base + lane;
-        const uint32_t word = w < p.words ? nb[w] : 0u;
-        const uint32_t c = __popc(word);
-        uint32_t incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= (unsigned)o) incl += x;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (!total) continue;
-        unsigned int off = 0;
-        if (lane == 0) off = atomicAdd(&cnt->conv_count, total);
-        off = __shfl_sync(0xffffffffu, off, 0);
-        uint32_t pos = off + incl - c;
-        uint32_t bits = word;
-        while (bits) {
-          const int b = __ffs(bits) - 1;
-          bits &= bits - 1;
-          q[pos++] = w * 32 + b;
-        }
-      }
+      compact_bitmap(p.bm[fcur ^ 1], p.queue[qcur], p.words, &cnt->conv_count, false);
       bar.sync();
       qlen = *(volatile unsigned int*)&cnt->conv_count;
     }

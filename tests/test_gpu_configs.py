@@ -1,0 +1,103 @@
+"""BASELINE.json configs on the B200: config 1 (RMAT-20, int32 offsets) for
+all 64 seeded sources against the oracle's serial BFS, configs 2-3 (ER 2^24,
+4096^2 mesh) on seeded sources, plus size-independent BFS properties
+(checked vectorised over every arc) that also cover RMAT-26 when
+PBFS_TEST_LARGE=1."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2503_00430_b200 as pb
+
+pytestmark = pytest.mark.gpu
+UNREACHED = 0xFFFFFFFF
+
+
+def bfs_properties(g, dist, source):
+    """dist is a BFS layering of the component of `source`: dist[src] = 0,
+    no arc crosses more than one level or leaves the reached set, and every
+    reached vertex but the source has a neighbour one level closer."""
+    assert dist[source] == 0
+    deg = g.degrees()
+    d64 = dist.astype(np.int64)
+    d64[dist == UNREACHED] = -1
+    src = np.repeat(np.arange(g.vertex_count, dtype=np.int64), deg)
+    du, dv = d64[src], d64[g.column_indices]
+    assert ((du < 0) == (dv < 0)).all(), "an arc leaves the reached set"
+    both = du >= 0
+    assert (np.abs(du[both] - dv[both]) <= 1).all(), "an arc skips a level"
+    big = np.iinfo(np.int64).max
+    nb = np.where(dv >= 0, dv, big)
+    has = deg > 0
+    mins = np.full(g.vertex_count, big, dtype=np.int64)
+    mins[has] = np.minimum.reduceat(nb, g.row_offsets[:-1][has].astype(np.int64))
+    reached = d64 > 0
+    assert (mins[reached] == d64[reached] - 1).all(), "a vertex lacks a parent"
+
+
+def config_graph(name):
+    if name == "rmat20":
+        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 20, 16, 1,
+                                            drop_self_loops=True)), 4
+    if name == "er24":
+        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.UniformRandom, 24, 16, 1,
+                                            drop_self_loops=True)), 8
+    if name == "mesh4096":
+        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Mesh, seed=1, mesh_side=4096,
+                                            drop_self_loops=True)), 8
+    if name == "rmat26":
+        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 26, 16, 1,
+                                            drop_self_loops=True)), 8
+    raise KeyError(name)
+
+
+def dispatch_config(g):
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid)
+    if pb.compute_stats(g).category == pb.GraphCategory.LargeDiameter:
+        cfg.force_top_down_only = True
+    return cfg
+
+
+def test_config1_rmat20_all_64_sources(port):
+    g, offb = config_graph("rmat20")
+    dg = g.device(0, offb)
+    assert dg.info["device_offset_bytes"] == 4
+    cfg = dispatch_config(g)
+    for i, s in enumerate(pb.pick_sources(g, 64, 1)):
+        want = port.bfs_serial(g.row_offsets, g.column_indices, int(s))
+        got = dg.bfs(int(s), cfg).distances
+        assert np.array_equal(got, want), int(s)
+        if i < 8:
+            for v in (pb.KernelVariant.Conventional, pb.KernelVariant.NonAtomic,
+                      pb.KernelVariant.HybridBeamer):
+                assert np.array_equal(dg.bfs(int(s), pb.KernelConfig(variant=v)).distances,
+                                      want)
+    bfs_properties(g, got, int(s))
+
+
+@pytest.mark.parametrize("name", ["er24", "mesh4096"])
+def test_config2_config3_seeded_sources(name, port):
+    g, offb = config_graph(name)
+    dg = g.device(0, offb)
+    cfg = dispatch_config(g)
+    if name == "mesh4096":
+        assert cfg.force_top_down_only  # avg degree ~3.6 -> the dispatcher's TD-only path
+    for s in pb.pick_sources(g, 3, 1):
+        want = port.bfs_serial(g.row_offsets, g.column_indices, int(s))
+        r = dg.bfs(int(s), cfg)
+        assert np.array_equal(r.distances, want), (name, int(s))
+        assert sum(rec.distinct_size for rec in r.trace.records) == \
+            int((want != UNREACHED).sum())
+    bfs_properties(g, r.distances, int(s))
+    g.release_device()
+
+
+@pytest.mark.skipif(os.environ.get("PBFS_TEST_LARGE") != "1", reason="set PBFS_TEST_LARGE=1")
+def test_config4_rmat26_properties():
+    g, offb = config_graph("rmat26")
+    dg = g.device(0, offb)
+    cfg = dispatch_config(g)
+    for s in pb.pick_sources(g, 2, 1):
+        r = dg.bfs(int(s), cfg)
+        bfs_properties(g, r.distances, int(s))

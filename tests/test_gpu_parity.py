@@ -1,0 +1,295 @@
+"""GPU parity: every traversal runs on the B200 through the C ABI
+(libpbfs.so) and is compared bit-exactly with the CPU oracle (serial BFS /
+relaxation restated from the reference, pinned by tests/test_oracle.py) and
+with the reference's own golden vectors. Mirrors test_kernels.cpp and
+acceptance.cpp criteria 1, 2 and 4."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_2503_00430_b200 as pb
+from graphs import (from_edges, hand_suite, make_circulant, make_complete_bipartite,
+                    make_clique, make_edgeless, make_path, make_star, random_graph)
+
+pytestmark = pytest.mark.gpu
+UNREACHED = 0xFFFFFFFF
+V = pb.KernelVariant
+GPU_VARIANTS = [V.Conventional, V.NonAtomic, V.Hybrid, V.HybridBeamer, V.VisitedBitmapInline]
+DIRECT = {V.Conventional: pb.bfs_conventional, V.NonAtomic: pb.bfs_nonatomic,
+          V.Hybrid: pb.bfs_hybrid, V.HybridBeamer: pb.bfs_hybrid_beamer,
+          V.VisitedBitmapInline: lambda g, s, c: pb.bfs_visited_bitmap(g, s, c, False)}
+
+
+def run(variant, g, s, **kw):
+    cfg = pb.KernelConfig(variant=variant, **kw)
+    return DIRECT[variant](g, s, cfg)
+
+
+def check_trace_shape(r, dist, source):
+    # test_kernels.cpp:53-66
+    assert r.trace.source == source
+    total = 0
+    for i, rec in enumerate(r.trace.records):
+        assert rec.depth == i
+        assert rec.frontier_size == rec.distinct_size + rec.duplicate_count
+        total += rec.distinct_size
+    assert total == int((dist != UNREACHED).sum())
+
+
+def phases(r):
+    return [int(rec.phase) for rec in r.trace.records]
+
+
+@pytest.mark.parametrize("variant", GPU_VARIANTS, ids=lambda v: pb.to_string(v))
+def test_hand_graphs_match_relaxation(variant, port):
+    # test_kernels.cpp:129-166
+    for name, g, s in hand_suite():
+        want = port.relaxation(g.row_offsets, g.column_indices, s)
+        r = run(variant, g, s)
+        assert np.array_equal(r.distances, want), name
+        assert r.trace.variant == variant
+        check_trace_shape(r, r.distances, s)
+
+
+@pytest.mark.parametrize("offset_bytes", [4, 8])
+def test_acceptance_criterion_1_generated_graphs(offset_bytes, port):
+    # acceptance.cpp:112-147: 200 graphs, 5 sources each, every GPU variant
+    runs = 0
+    for i in range(200):
+        kind = pb.GeneratorKind.UniformRandom if i % 2 == 0 else pb.GeneratorKind.Kronecker
+        spec = pb.GeneratorSpec(kind, 4 + i % 9, 1 + (i * 5) % 16, 7000 + i)
+        g = pb.generate(spec)
+        dg = g.device(0, offset_bytes)
+        raw = port.mt64(i, 4096)
+        deg = g.degrees()
+        sources = [int(v) for v in (raw % np.uint64(g.vertex_count)) if deg[int(v)] > 0][:5]
+        for s in sources:
+            want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+            for variant in GPU_VARIANTS:
+                r = dg.bfs(s, pb.KernelConfig(variant=variant))
+                runs += 1
+                assert np.array_equal(r.distances, want), (pb.to_string(spec), s, variant)
+        g.release_device()
+    assert runs >= 4500
+
+
+def test_golden_vectors_from_reference(golden_dir):
+    # distances and per-level phases produced by the reference library itself
+    for path in sorted(glob.glob(os.path.join(golden_dir, "gen_*.npz"))):
+        gold = np.load(path)
+        kind, scale, ef, seed = os.path.basename(path)[4:-4].split("_")
+        g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker if kind == "kron"
+                                         else pb.GeneratorKind.UniformRandom,
+                                         int(scale), int(ef), int(seed)))
+        for s in gold["sources"]:
+            s = int(s)
+            if f"dist_{s}" not in gold:
+                continue
+            r = run(V.Hybrid, g, s)
+            assert np.array_equal(r.distances, gold[f"dist_{s}"]), (path, s)
+            assert phases(r) == gold[f"hybrid_phase_{s}"].tolist(), (path, s)
+            assert [rec.distinct_size for rec in r.trace.records] == \
+                gold[f"hybrid_distinct_{s}"].tolist()
+            rb = run(V.HybridBeamer, g, s)
+            assert np.array_equal(rb.distances, gold[f"dist_{s}"])
+            assert phases(rb) == gold[f"beamer_phase_{s}"].tolist(), (path, s)
+            rc = run(V.Conventional, g, s)
+            assert np.array_equal(rc.distances, gold[f"dist_{s}"])
+
+
+def test_star_frontier_series_and_edges():
+    # test_kernels.cpp:168-184
+    r = run(V.Conventional, make_star(64), 0)
+    assert pb.frontier_size_series(r.trace) == [(0, 1), (1, 64)]
+    assert [rec.duplicate_count for rec in r.trace.records] == [0, 0]
+    assert [rec.edges_examined for rec in r.trace.records] == [64, 64]
+
+
+def test_zero_degree_source_single_level():
+    # test_kernels.cpp:186-197
+    r = run(V.Conventional, make_edgeless(5), 3)
+    assert r.distances.tolist() == [UNREACHED] * 3 + [0, UNREACHED]
+    assert len(r.trace.records) == 1
+    assert r.trace.records[0].frontier_size == 1 and r.trace.records[0].edges_examined == 0
+
+
+def test_small_dense_graph_bottom_up_from_seed(port):
+    # test_kernels.cpp:199-211
+    g = make_star(16)
+    r = run(V.Hybrid, g, 0)
+    assert r.trace.records[0].phase == pb.TraversalPhase.BottomUp
+    assert r.trace.level_count(pb.TraversalPhase.BottomUp) == len(r.trace.records)
+    assert np.array_equal(r.distances, port.relaxation(g.row_offsets, g.column_indices, 0))
+
+
+def test_threshold_one_keeps_hybrid_top_down():
+    # test_kernels.cpp:213-232
+    g = make_path(10)
+    plain = run(V.NonAtomic, g, 0)
+    hyb = run(V.Hybrid, g, 0, hybrid_threshold_fraction=1.0)
+    assert hyb.trace.level_count(pb.TraversalPhase.BottomUp) == 0
+    assert np.array_equal(hyb.distances, plain.distances)
+    assert phases(hyb) == phases(plain)
+    assert [r.distinct_size for r in hyb.trace.records] == \
+        [r.distinct_size for r in plain.trace.records]
+
+
+def test_long_path_stays_top_down(port):
+    # test_kernels.cpp:234-242
+    g = make_path(1000)
+    r = run(V.Hybrid, g, 0)
+    assert len(r.trace.records) == 1000
+    assert r.trace.level_count(pb.TraversalPhase.BottomUp) == 0
+    assert np.array_equal(r.distances, port.relaxation(g.row_offsets, g.column_indices, 0))
+
+
+def test_phases_follow_replayed_rules(port):
+    # test_kernels.cpp:244-283 (size fraction and edge count)
+    items = [(make_circulant(100, [2, 3, 50]), 0), (make_complete_bipartite(8, 64), 0),
+             (random_graph(200, 1400, 21), 0), (make_path(10), 0),
+             (make_circulant(100, [2, 3, 50]), 7),
+             (pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 10, 8, 77)), 0)]
+    for g, s in items:
+        if g.degree(s) == 0:
+            s = int(np.argmax(g.degrees()))
+        dist = port.bfs_serial(g.row_offsets, g.column_indices, s)
+        r = run(V.Hybrid, g, s)
+        assert phases(r) == port.simulate_phases(g.row_offsets, dist)
+        rb = run(V.HybridBeamer, g, s)
+        assert phases(rb) == port.simulate_phases(g.row_offsets, dist, beamer=True)
+        assert np.array_equal(r.distances, dist) and np.array_equal(rb.distances, dist)
+
+
+def test_beamer_policy_limits(port):
+    # test_kernels.cpp:285-309
+    g = make_circulant(100, [2, 3, 50])
+    dist = port.bfs_serial(g.row_offsets, g.column_indices, 0)
+    r = run(V.HybridBeamer, g, 0, alpha=1e-9)
+    assert phases(r) == port.simulate_phases(g.row_offsets, dist, beamer=True, alpha=1e-9)
+    assert all(p == 0 for p in phases(r)[:-1]) and phases(r)[-1] == 1
+    r = run(V.HybridBeamer, g, 0, alpha=1e9)
+    assert phases(r)[0] == 1
+    assert phases(r) == port.simulate_phases(g.row_offsets, dist, beamer=True, alpha=1e9)
+
+
+def test_hybrid_examines_fewer_edges_than_conventional(port):
+    # test_kernels.cpp:311-326
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 12, 16, 3))
+    src = int(np.argmax(g.degrees()))
+    want = port.bfs_serial(g.row_offsets, g.column_indices, src)
+    conv = run(V.Conventional, g, src)
+    hyb = run(V.Hybrid, g, src)
+    assert np.array_equal(conv.distances, want) and np.array_equal(hyb.distances, want)
+    assert hyb.trace.level_count(pb.TraversalPhase.BottomUp) >= 1
+    assert phases(hyb) == port.simulate_phases(g.row_offsets, want)
+    assert hyb.trace.total_edges_examined() < conv.trace.total_edges_examined()
+
+
+def test_symmetry_requirement_and_directed_top_down():
+    # test_kernels.cpp:423-449
+    chain = from_edges([(0, 1), (1, 2)], 3, symmetrize=False)
+    assert not chain.symmetric
+    for v in (V.Hybrid, V.HybridBeamer, V.VisitedBitmapInline):
+        with pytest.raises(pb.InputError, match="symmetric"):
+            run(v, chain, 0)
+    r = run(V.Hybrid, chain, 0, force_top_down_only=True)
+    assert r.distances.tolist() == [0, 1, 2]
+    assert r.trace.level_count(pb.TraversalPhase.BottomUp) == 0
+    assert run(V.Conventional, chain, 0).distances.tolist() == [0, 1, 2]
+    assert run(V.NonAtomic, chain, 2).distances.tolist() == [UNREACHED, UNREACHED, 0]
+
+
+def test_dispatcher_forces_sparse_graphs_top_down(port):
+    # test_kernels.cpp:451-497
+    edges = [(i, (i + 1) % 100) for i in range(100)] + [(i, i + 50) for i in range(33)]
+    g = from_edges(edges, 100)
+    st = pb.compute_stats(g)
+    assert st.average_degree == pytest.approx(2.66)
+    assert st.category == pb.GraphCategory.LargeDiameter
+    cfg = pb.KernelConfig(variant=V.Hybrid)
+    d = pb.run_bfs(g, 0, cfg, st)
+    assert d.trace.level_count(pb.TraversalPhase.BottomUp) == 0
+    assert np.array_equal(d.distances, port.relaxation(g.row_offsets, g.column_indices, 0))
+    direct = pb.bfs_hybrid(g, 0, cfg)
+    assert phases(direct) == port.simulate_phases(g.row_offsets, d.distances)
+    star = make_star(40)
+    forced = pb.run_bfs(star, 0, cfg, pb.compute_stats(star))
+    assert forced.trace.level_count(pb.TraversalPhase.BottomUp) == 0
+    free = pb.bfs_hybrid(star, 0, cfg)
+    assert free.trace.level_count(pb.TraversalPhase.BottomUp) == 1
+    dense = make_circulant(100, [2, 3, 4, 5, 6, 7, 50])
+    r = pb.run_bfs(dense, 0, cfg, pb.compute_stats(dense))
+    assert r.trace.level_count(pb.TraversalPhase.BottomUp) >= 1
+
+
+def test_errors_map_to_reference_exceptions():
+    # test_kernels.cpp:120-127; variants without a GPU form
+    g = make_path(3)
+    with pytest.raises(pb.InputError):
+        run(V.Conventional, g, 99)
+    with pytest.raises(pb.InputError):
+        pb.run_bfs(g, 3, pb.KernelConfig(variant=V.Hybrid), pb.compute_stats(g))
+    for v in (V.Serial, V.VisitedBitmapDeferred, V.TopDownPeriodicFlush):
+        with pytest.raises(pb.ConfigError):
+            pb.run_bfs(g, 0, pb.KernelConfig(variant=v), pb.compute_stats(g))
+    with pytest.raises(pb.ConfigError):
+        run(V.Hybrid, g, 0, hybrid_threshold_fraction=0.0)
+
+
+def test_same_value_stores_and_duplicates(port):
+    # acceptance.cpp:151-186, test_kernels.cpp:553-564
+    for g in (random_graph(128, 700, 31), make_clique(24), make_complete_bipartite(16, 16)):
+        r = run(V.NonAtomic, g, 0, validate_same_value_stores=True)
+        assert r.trace.same_value_violations == 0
+        assert np.array_equal(r.distances, port.relaxation(g.row_offsets, g.column_indices, 0))
+        check_trace_shape(r, r.distances, 0)
+
+
+def test_top_down_edges_equal_reached_degree_sum():
+    # test_kernels.cpp:566-576
+    g = random_graph(160, 900, 13)
+    r = run(V.Conventional, g, 2)
+    want = int(g.degrees()[r.distances != UNREACHED].sum())
+    assert r.trace.total_edges_examined() == want
+
+
+def test_repeated_and_interleaved_traversals_are_independent(port):
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 14, 16, 5,
+                                     drop_self_loops=True))
+    dg = g.device(0, 8)
+    srcs = [int(s) for s in pb.pick_sources(g, 6, 2)]
+    want = {s: port.bfs_serial(g.row_offsets, g.column_indices, s) for s in srcs}
+    for _ in range(3):
+        for s in srcs:
+            for v in GPU_VARIANTS:
+                assert np.array_equal(dg.bfs(s, pb.KernelConfig(variant=v)).distances, want[s])
+
+
+def test_async_api_and_device_component(port):
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 14, 16, 1,
+                                     drop_self_loops=True))
+    dg = g.device(0, 4)
+    s = int(pb.pick_sources(g, 1, 1)[0])
+    dg.bfs_async(s, pb.KernelConfig(variant=V.Hybrid))
+    dg.sync()
+    nr, ar = dg.component()
+    want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+    assert (nr, ar) == port.component(g.row_offsets, want)
+
+
+def test_time_run_checks_every_run(port):
+    # timing.cpp:33-69 and test_instrumentation.cpp:168-198 (fault injection)
+    g = make_circulant(64, [3])
+    want = port.bfs_serial(g.row_offsets, g.column_indices, 0)
+    rep = pb.time_run(g, 0, pb.KernelConfig(variant=V.Hybrid), 3, 1, pb.compute_stats(g), want)
+    assert len(rep.samples_ns) == 3 and rep.median_ns in rep.samples_ns
+
+    def broken(gr, s, c):
+        r = pb.bfs_hybrid(gr, s, c)
+        r.distances = r.distances.copy()
+        r.distances[5] += 1
+        return r
+    with pytest.raises(pb.CorrectnessError, match="vertex 5"):
+        pb.time_run(g, 0, pb.KernelConfig(variant=V.Hybrid), 1, 0, broken, want)

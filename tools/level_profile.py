@@ -27,4 +27,5 @@ for s in pb.pick_sources(g, args.sources, 1):
     for rec in t.records:
         print(f"  d={rec.depth:3d} {pb.to_string(rec.phase):9s} frontier={rec.frontier_size:10d} "
               f"distinct={rec.distinct_size:10d} edges={rec.edges_examined:12d} "
-              f"t={rec.elapsed_ns/1e3:9.1f} us")
+              f"t={rec.elapsed_ns/1e3:9.1f} us  light={rec.flush_events & 0xffffffff} us "
+              f"items={rec.flush_events >> 32}")
