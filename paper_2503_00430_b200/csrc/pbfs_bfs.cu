@@ -208,6 +208,9 @@ int occupancy_for(int claim) {
   const void* fn = claim == kClaimCas     ? reinterpret_cast<const void*>(&bfs_persistent<kClaimCas, OffT>)
                    : claim == kClaimPlain ? reinterpret_cast<const void*>(&bfs_persistent<kClaimPlain, OffT>)
                                           : reinterpret_cast<const void*>(&bfs_persistent<kClaimBitmap, OffT>);
+  // Smallest shared-memory carveout that fits the resident CTAs: the rest of
+  // the 228 KB stays L1, which caches the frozen visited-bitmap probes.
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0);
   return blocks;
 }
@@ -316,7 +319,9 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   g->symmetric = csr->symmetric != 0;
   // Host-side per-graph facts: max degree, heavy-item capacity, the
   // zero-degree mask that lets bottom-up skip isolated vertices.
-  g->words = static_cast<uint32_t>(((n + 31) / 32 + kGroupWords - 1) / kGroupWords * kGroupWords);
+  // Whole 32-word groups: bottom-up takes 16-word groups, the merge and
+  // compaction passes 32-word warp groups.
+  g->words = static_cast<uint32_t>(((n + 31) / 32 + 31) / 32 * 32);
   if (g->words == 0) g->words = kGroupWords;
   std::vector<uint32_t> mask(g->words, 0);
   {

@@ -39,12 +39,19 @@ namespace dev {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef PBFS_MIN_BLOCKS
+#define PBFS_MIN_BLOCKS 3
+#endif
+constexpr int kMinBlocks = PBFS_MIN_BLOCKS;  // resident CTAs per SM the register budget targets
 constexpr uint32_t kHeavyDeg = 1024; // degree above which a vertex is split
 constexpr uint32_t kChunk = 2048;    // edges per heavy work item
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
+// Top-down frontiers at least this large write a next-frontier bitmap (no
+// claim atomics with return, ordered distance writes) instead of a queue.
+constexpr unsigned long long kBitmapMinFrontier = 4096;
 
 enum Claim : int { kClaimCas = 0, kClaimPlain = 1, kClaimBitmap = 2 };
 enum Policy : int { kPolicyTopDown = 0, kPolicyFraction = 1, kPolicyBeamer = 2 };
@@ -152,6 +159,19 @@ __device__ __forceinline__ uint32_t atom_cas_if(bool pred, uint32_t* addr, uint3
       : "+r"(old)
       : "l"(addr), "r"((uint32_t)pred), "r"(cmp), "r"(val));
   return old;
+}
+__device__ __forceinline__ uint32_t ld_cg_if(bool pred, const uint32_t* addr, uint32_t dflt) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q ld.global.cg.u32 %0, [%2];\n\t}"
+      : "+r"(dflt)
+      : "r"((uint32_t)pred), "l"(addr));
+  return dflt;
+}
+__device__ __forceinline__ void red_or_if(bool pred, uint32_t* addr, uint32_t val) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+      "@q red.global.or.b32 [%1], %2;\n\t}" ::"r"((uint32_t)pred), "l"(addr), "r"(val));
 }
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
@@ -269,7 +289,31 @@ template <int C, int K, typename OffT>
 __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
                                             const uint32_t (&v)[K], uint32_t okm,
                                             uint32_t* qout, WarpPush& wp, LevelCnt* cnt,
-                                            WarpTally& t) {
+                                            WarpTally& t, uint32_t* obm) {
+  if constexpr (C == kClaimBitmap) {
+    if (obm) {
+      // Bitmap-output top-down (large frontiers): `visited` is frozen for the
+      // whole level, so its probe may come from L1 (hub words stay hot);
+      // only a miss there is re-probed at L2 in the output bitmap, and only a
+      // miss there too issues a no-return red.or. Every racing discoverer
+      // sets the same bit (idempotent, like the reference's same-value byte
+      // stores); distances and the queue are produced afterwards, in vertex
+      // order, by the merge pass. No atomic result is waited on here.
+      uint32_t w[K], o[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) w[k] = __ldca(&p.visited[v[k] >> 5]);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const bool miss = ((okm >> k) & 1u) && !((w[k] >> (v[k] & 31)) & 1u);
+        o[k] = ld_cg_if(miss, &obm[v[k] >> 5], 0xffffffffu);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        red_or_if(!((o[k] >> (v[k] & 31)) & 1u), &obm[v[k] >> 5], 1u << (v[k] & 31));
+      }
+      return;
+    }
+  }
   // Unconditional probes (dead slots hold a valid vertex id): predicated
   // loads end up in separate blocks that ptxas interleaves with their uses,
   // serialising the round trips this batching exists to overlap.
@@ -336,7 +380,7 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
 template <int C, typename OffT>
 __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t nd, OffT beg,
                                                uint32_t deg, uint32_t* qout, WarpPush& wp,
-                                               LevelCnt* cnt, WarpTally& t) {
+                                               LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
   constexpr int K = 16;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -372,7 +416,7 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
       const unsigned long long ei = ok ? (unsigned long long)ob + (e - oex) : (unsigned long long)b0;
       v[k] = __ldcs(&p.col[ei]);
     }
-    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t);
+    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
   }
 }
 
@@ -381,7 +425,7 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
 template <int C, typename OffT>
 __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint32_t* qin,
                                unsigned long long qlen, uint32_t* qout, WarpPush& wp,
-                               LevelCnt* cnt, WarpTally& t) {
+                               LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
@@ -426,7 +470,7 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
       }
     }
     if (hub) deg = 0;
-    td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t);
+    td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t, obm);
     unsigned int nb = 0;
     if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
     base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
@@ -441,7 +485,8 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
 // DRAM, is what bounds a random-probe loop on this part.
 template <int C, typename OffT>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
-                               uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t) {
+                               uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t,
+                               uint32_t* obm) {
   constexpr int K = 16;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -462,7 +507,7 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
         okm |= (uint32_t)ok << k;
         v[k] = __ldcs(&base[ok ? e : 0u]);
       }
-      claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t);
+      claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
     }
     // Items are equal-sized (kChunk edges but a hub's last one): a static
     // round-robin balances them without a contended cursor.
@@ -585,11 +630,53 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
   t = WarpTally{};
 }
 
+// After a bitmap-mode top-down level: visited |= frontier, dist = d+1 for
+// every new vertex (warp-transposed so each store instruction covers one
+// 128 B run of dist), distinct count into cnt->conv_count, Beamer degree sum,
+// and the stale bitmap zeroed (restores the bm[fcur ^ 1] == 0 invariant).
+template <typename OffT>
+__device__ __forceinline__ void merge_frontier(const Params<OffT>& p, const uint32_t* fb,
+                                               uint32_t* stale, uint32_t nd, LevelCnt* cnt) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = lane_id();
+  const unsigned warps_total = gridDim.x * kWarps;
+  const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  unsigned long long count = 0, degsum = 0;
+  for (uint32_t base = gw * 32; base < p.words; base += warps_total * 32) {
+    const uint32_t w = base + lane;
+    const uint32_t word = fb[w];
+    stale[w] = 0;
+    if (word) p.visited[w] |= word;
+    count += __popc(word);
+    unsigned nz = __ballot_sync(FULL, word != 0);
+    while (nz) {
+      const int j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t wj = __shfl_sync(FULL, word, j);
+      const uint32_t v = (base + j) * 32 + lane;
+      if ((wj >> lane) & 1u) {
+        p.dist[v] = nd;
+        if (p.policy == kPolicyBeamer) degsum += degree_of(p, v);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    count += __shfl_xor_sync(FULL, count, o);
+    degsum += __shfl_xor_sync(FULL, degsum, o);
+  }
+  if (lane == 0) {
+    if (count) atomicAdd(&cnt->conv_count, (unsigned int)count);
+    if (degsum) atomicAdd(&cnt->degree, degsum);
+  }
+}
+
 // Bitmap -> queue (count_bitmap_slice / write_dense_slice, kernels.cpp:
 // 225-241): each warp compacts 32 words with a popcount scan and reserves its
 // output range with one atomicAdd; optionally clears the words it consumed.
 __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
-                                               unsigned int* counter, bool clear) {
+                                               unsigned int* counter, bool clear,
+                                               uint32_t* zero_other = nullptr) {
   const unsigned lane = lane_id();
   const unsigned warps_total = gridDim.x * kWarps;
   const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -597,6 +684,7 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
     const uint32_t w = base + lane;
     const uint32_t word = w < words ? nb[w] : 0u;
     if (clear && word) nb[w] = 0;
+    if (zero_other && w < words) zero_other[w] = 0;
     const uint32_t c = __popc(word);
     uint32_t incl = c;
 #pragma unroll
@@ -620,7 +708,7 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
 }
 
 template <int C, typename OffT>
-__global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
   __shared__ uint32_t s_list[kWarps][kGroupVerts];  // BU id list / TD push buffer
   __shared__ uint32_t s_found[kWarps][kGroupWords];
   const unsigned warp = threadIdx.x >> 5;
@@ -682,6 +770,10 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
   unsigned long long t_start = leader ? globaltimer() : 0;
   bar.sync();
 
+  // Bitmap bookkeeping. bm[fcur] holds the latest frontier whenever it is in
+  // bitmap form; invariant: bm[fcur ^ 1] is all-zero whenever a top-down
+  // level starts (it is the output of a bitmap-mode top-down level and the
+  // mark target when a queue-mode level hands over to bottom-up).
   uint32_t depth = 0;
   for (;; ++depth) {
     LevelCnt* cnt = &ctl->cnt[depth & 3];
@@ -690,10 +782,13 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
       ctl->cnt[(depth + 2) & 3] = z;
     }
     WarpTally t;
+    // Large top-down frontiers take the bitmap-output path (C == kClaimBitmap).
+    const bool bm_mode = C == kClaimBitmap && td && qlen >= kBitmapMinFrontier;
     unsigned long long dbg_mid = 0, dbg_items = 0;
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
-      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t);
+      uint32_t* obm = bm_mode ? p.bm[fcur ^ 1] : nullptr;
+      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, obm);
       if (p.max_degree > kHeavyDeg) {
         bar.sync();
         const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
@@ -701,7 +796,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
           dbg_mid = globaltimer();
           dbg_items = items;
         }
-        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t);
+        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, obm);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
@@ -714,12 +809,20 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
       compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true);
       bar.sync();
     }
+    if (bm_mode) {
+      // Merge: visited |= new frontier, distances in vertex order, distinct
+      // count (and Beamer degree sum); clears the stale bitmap.
+      merge_frontier(p, p.bm[fcur ^ 1], p.bm[fcur], depth + 1, cnt);
+      bar.sync();
+      fcur ^= 1;
+    }
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
     const unsigned long long produced =
-        C == kClaimPlain ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
-                         : *(volatile unsigned long long*)&cnt->produced;
-    const unsigned long long raw = td ? *(volatile unsigned long long*)&cnt->raw : produced;
+        (C == kClaimPlain || bm_mode) ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
+                                      : *(volatile unsigned long long*)&cnt->produced;
+    const unsigned long long raw =
+        (td && !bm_mode) ? *(volatile unsigned long long*)&cnt->raw : produced;
     const unsigned long long edges = *(volatile unsigned long long*)&cnt->edges;
     const unsigned long long pdeg = *(volatile unsigned long long*)&cnt->degree;
     const unsigned int overflow = *(volatile unsigned int*)&ctl->overflow;
@@ -748,27 +851,36 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(Params<OffT> p) {
     unvisited_edges -= pdeg;
     const unsigned long long consumed = cur_distinct;
     const bool next_td = decide(td, produced, pdeg, consumed, unvisited_edges);
+    if (!td) fcur ^= 1;  // bottom-up output becomes the latest frontier
     if (td && next_td) {
-      qcur ^= 1;
-      qlen = C == kClaimPlain ? produced : raw;
-    } else if (!td && !next_td) {
-      fcur ^= 1;
-    } else if (td && !next_td) {
-      // Entering bottom-up: frontier bitmap from the produced queue
-      // (mark_bitmap_from_dense, kernels.cpp:243-260).
-      uint32_t* fb = p.bm[fcur];
-      for (unsigned long long w = tid; w < p.words; w += nthreads) fb[w] = 0;
-      bar.sync();
-      const uint32_t* q = p.queue[qcur ^ 1];
-      for (unsigned long long i = tid; i < raw; i += nthreads) {
-        const uint32_t v = q[i];
-        atomicOr(&fb[v >> 5], 1u << (v & 31));
+      if (bm_mode) {
+        compact_bitmap(p.bm[fcur], p.queue[qcur ^ 1], p.words, &cnt->mark_cursor, false);
+        bar.sync();
+        qlen = *(volatile unsigned int*)&cnt->mark_cursor;
+      } else {
+        qlen = C == kClaimPlain ? produced : raw;
       }
-      bar.sync();
-    } else {
+      qcur ^= 1;
+    } else if (td && !next_td) {
+      if (!bm_mode) {
+        // Entering bottom-up from a queue (mark_bitmap_from_dense,
+        // kernels.cpp:243-260) into bm[fcur ^ 1], zero by the invariant.
+        uint32_t* fb = p.bm[fcur ^ 1];
+        const uint32_t* q = p.queue[qcur ^ 1];
+        for (unsigned long long i = tid; i < raw; i += nthreads) {
+          const uint32_t v = q[i];
+          atomicOr(&fb[v >> 5], 1u << (v & 31));
+        }
+        bar.sync();
+        fcur ^= 1;
+      }
+      // bitmap mode: bm[fcur] already is the frontier, visited is merged.
+    } else if (!td && next_td) {
       // Entering top-down: ascending queue from the produced bitmap
-      // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241).
-      compact_bitmap(p.bm[fcur ^ 1], p.queue[qcur], p.words, &cnt->conv_count, false);
+      // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241); the
+      // stale bitmap is cleared on the way to restore the invariant.
+      compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false,
+                     p.bm[fcur ^ 1]);
       bar.sync();
       qlen = *(volatile unsigned int*)&cnt->conv_count;
     }

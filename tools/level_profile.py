@@ -19,7 +19,7 @@ g = bench.build_graph(args.workload)
 cfg, _ = bench.kernel_config(g)
 cfg.variant = pb.parse_kernel_variant(args.variant)
 dg = g.device(0, bench.WORKLOADS[args.workload][3])
-for s in pb.pick_sources(g, args.sources, 1):
+for s in pb.pick_sources(g, min(args.sources, 3), 1):
     dg.bfs(int(s), cfg, want_trace=False)  # warm
     r = dg.bfs(int(s), cfg)
     t = r.trace
@@ -29,3 +29,21 @@ for s in pb.pick_sources(g, args.sources, 1):
               f"distinct={rec.distinct_size:10d} edges={rec.edges_examined:12d} "
               f"t={rec.elapsed_ns/1e3:9.1f} us  light={rec.flush_events & 0xffffffff} us "
               f"items={rec.flush_events >> 32}")
+
+if args.sources >= 16:
+    # Aggregate: where does the time go across sources (by phase and size).
+    import collections
+    agg = collections.Counter()
+    times = []
+    for s in pb.pick_sources(g, args.sources, 1):
+        r = dg.bfs(int(s), cfg)
+        times.append(r.trace.device_ms)
+        for rec in r.trace.records:
+            big = rec.edges_examined > 1e7 or rec.frontier_size > 1e6
+            key = f"{pb.to_string(rec.phase)}-{'big' if big else 'small'}"
+            agg[key] += rec.elapsed_ns / 1e6
+    times.sort()
+    print("per-source ms: min %.3f p50 %.3f p90 %.3f max %.3f sum %.1f" % (
+        times[0], times[len(times) // 2], times[int(len(times) * 0.9)], times[-1], sum(times)))
+    for k, v in sorted(agg.items()):
+        print(f"  {k:18s} {v:9.2f} ms total")
