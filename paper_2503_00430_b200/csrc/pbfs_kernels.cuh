@@ -784,7 +784,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     WarpTally t;
     // Large top-down frontiers take the bitmap-output path (C == kClaimBitmap).
     const bool bm_mode = C == kClaimBitmap && td && qlen >= kBitmapMinFrontier;
-    unsigned long long dbg_mid = 0, dbg_items = 0;
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
       uint32_t* obm = bm_mode ? p.bm[fcur ^ 1] : nullptr;
@@ -792,10 +791,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       if (p.max_degree > kHeavyDeg) {
         bar.sync();
         const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
-        if (leader) {
-          dbg_mid = globaltimer();
-          dbg_items = items;
-        }
         if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, obm);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
@@ -836,8 +831,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
         r.distinct_size = cur_distinct;
         r.duplicate_count = cur_raw - cur_distinct;
         r.edges_examined = edges;
-        // DIAGNOSTIC (temporary): heavy items << 32 | light-phase microseconds
-        r.flush_events = dbg_mid ? (dbg_items << 32) | ((dbg_mid - t_start) / 1000) : 0;
+        r.flush_events = 0;  // no local-buffer flushes to report on the GPU
         r.elapsed_ns = (long long)(now - t_start);
         p.records[depth] = r;
       }

@@ -27,8 +27,7 @@ for s in pb.pick_sources(g, min(args.sources, 3), 1):
     for rec in t.records:
         print(f"  d={rec.depth:3d} {pb.to_string(rec.phase):9s} frontier={rec.frontier_size:10d} "
               f"distinct={rec.distinct_size:10d} edges={rec.edges_examined:12d} "
-              f"t={rec.elapsed_ns/1e3:9.1f} us  light={rec.flush_events & 0xffffffff} us "
-              f"items={rec.flush_events >> 32}")
+              f"t={rec.elapsed_ns/1e3:9.1f} us")
 
 if args.sources >= 16:
     # Aggregate: where does the time go across sources (by phase and size).
