@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpbfs.so")
+# PBFS_LIB overrides the library path (A/B builds of the same ABI).
+LIB_PATH = os.environ.get("PBFS_LIB", os.path.join(HERE, "libpbfs.so"))
 
 c_u32 = ctypes.c_uint32
 c_u64 = ctypes.c_uint64

@@ -42,6 +42,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_MIN_BLOCKS
 #define PBFS_MIN_BLOCKS 3
 #endif
+#ifndef PBFS_SLOTS
+#define PBFS_SLOTS 8  // edge slots per lane in the top-down batches
+#endif
 constexpr int kMinBlocks = PBFS_MIN_BLOCKS;  // resident CTAs per SM the register budget targets
 constexpr uint32_t kHeavyDeg = 1024; // degree above which a vertex is split
 constexpr uint32_t kChunk = 2048;    // edges per heavy work item
@@ -49,9 +52,6 @@ constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
-// Top-down frontiers at least this large write a next-frontier bitmap (no
-// claim atomics with return, ordered distance writes) instead of a queue.
-constexpr unsigned long long kBitmapMinFrontier = 4096;
 
 enum Claim : int { kClaimCas = 0, kClaimPlain = 1, kClaimBitmap = 2 };
 enum Policy : int { kPolicyTopDown = 0, kPolicyFraction = 1, kPolicyBeamer = 2 };
@@ -290,30 +290,6 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
                                             const uint32_t (&v)[K], uint32_t okm,
                                             uint32_t* qout, WarpPush& wp, LevelCnt* cnt,
                                             WarpTally& t, uint32_t* obm) {
-  if constexpr (C == kClaimBitmap) {
-    if (obm) {
-      // Bitmap-output top-down (large frontiers): `visited` is frozen for the
-      // whole level, so its probe may come from L1 (hub words stay hot);
-      // only a miss there is re-probed at L2 in the output bitmap, and only a
-      // miss there too issues a no-return red.or. Every racing discoverer
-      // sets the same bit (idempotent, like the reference's same-value byte
-      // stores); distances and the queue are produced afterwards, in vertex
-      // order, by the merge pass. No atomic result is waited on here.
-      uint32_t w[K], o[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) w[k] = __ldca(&p.visited[v[k] >> 5]);
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const bool miss = ((okm >> k) & 1u) && !((w[k] >> (v[k] & 31)) & 1u);
-        o[k] = ld_cg_if(miss, &obm[v[k] >> 5], 0xffffffffu);
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        red_or_if(!((o[k] >> (v[k] & 31)) & 1u), &obm[v[k] >> 5], 1u << (v[k] & 31));
-      }
-      return;
-    }
-  }
   // Unconditional probes (dead slots hold a valid vertex id): predicated
   // loads end up in separate blocks that ptxas interleaves with their uses,
   // serialising the round trips this batching exists to overlap.
@@ -361,6 +337,9 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
       winmask |= (uint32_t)won << k;
       if constexpr (C == kClaimBitmap) {
         if (won) p.dist[v[k]] = nd;
+        // Winners also mark the next-frontier bitmap (no-return red), so a
+        // switch to bottom-up needs no separate mark pass.
+        red_or_if(won, &obm[v[k] >> 5], 1u << (v[k] & 31));
       }
     }
     t.produced += __popc(winmask);
@@ -381,7 +360,7 @@ template <int C, typename OffT>
 __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t nd, OffT beg,
                                                uint32_t deg, uint32_t* qout, WarpPush& wp,
                                                LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
-  constexpr int K = 16;
+  constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   uint32_t incl = deg;
@@ -425,7 +404,7 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
 template <int C, typename OffT>
 __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint32_t* qin,
                                unsigned long long qlen, uint32_t* qout, WarpPush& wp,
-                               LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
+                               LevelCnt* cnt, WarpTally& t, uint32_t* obm, uint32_t* stale) {
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
@@ -438,6 +417,9 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
       const uint32_t u = qin[i];
       beg = __ldg(&p.rowptr[u]);
       end = __ldg(&p.rowptr[u + 1]);
+      // The stale bitmap's set bits are exactly this input frontier: zero
+      // their words so it can be the next level's mark target.
+      if (stale) stale[u >> 5] = 0;
     }
     unsigned long long deg = (unsigned long long)(end - beg);
     t.edges += deg;
@@ -487,7 +469,7 @@ template <int C, typename OffT>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
                                uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t,
                                uint32_t* obm) {
-  constexpr int K = 16;
+  constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
@@ -561,11 +543,13 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
     if (owner) found[lane] = 0;
     __syncwarp();
     for (uint32_t k = 0; k < total; k += 32 * KB) {
-      uint32_t v[KB], u[KB], fw[KB];
+      constexpr int C0 = 4;  // first chunk of neighbours per vertex
+      uint32_t v[KB], u[KB][C0], fw[KB][C0];
       OffT beg[KB], end[KB];
       bool valid[KB];
-      // Branch-free loads (dead slots read vertex list[0]'s data; `col` is
-      // padded so col[m] is readable) so ptxas keeps them overlapped.
+      // Branch-free loads (dead slots read vertex list[0]'s data, out-of-range
+      // neighbour slots re-read the first one; `col` is padded so col[m] is
+      // readable) so ptxas keeps every load of the batch in flight together.
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
         const uint32_t idx = k + 32 * q + lane;
@@ -575,28 +559,63 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
         end[q] = __ldg(&p.rowptr[v[q] + 1]);
       }
 #pragma unroll
-      for (int q = 0; q < KB; ++q) u[q] = __ldcs(&p.col[beg[q]]);
+      for (int q = 0; q < KB; ++q) {
+#pragma unroll
+        for (int c = 0; c < C0; ++c) {
+          const OffT e = beg[q] + c < end[q] ? beg[q] + c : beg[q];
+          u[q][c] = __ldcs(&p.col[e]);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
-        fw[q] = front[u[q] >> 5];
+#pragma unroll
+        for (int c = 0; c < C0; ++c) fw[q][c] = front[u[q][c] >> 5];
         if (!valid[q]) end[q] = beg[q];
       }
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
         if (beg[q] >= end[q]) continue;
-        bool hit = (fw[q] >> (u[q] & 31)) & 1u;
-        unsigned long long scanned = 1;
-        for (OffT e = beg[q] + 1; !hit && e < end[q]; ++e) {
-          const uint32_t x = __ldg(&p.col[e]);
-          ++scanned;
-          hit = (front[x >> 5] >> (x & 31)) & 1u;
+        // kernels.cpp:362-374: first frontier neighbour wins (early exit);
+        // edges count up to and including it.
+        const unsigned long long deg = (unsigned long long)(end[q] - beg[q]);
+        unsigned hitmask = 0;
+#pragma unroll
+        for (int c = 0; c < C0; ++c) {
+          hitmask |= (unsigned)((c < (long long)deg) && ((fw[q][c] >> (u[q][c] & 31)) & 1u)) << c;
+        }
+        unsigned long long scanned;
+        bool hit = hitmask != 0;
+        if (hit) {
+          scanned = (unsigned long long)__ffs(hitmask);
+        } else {
+          scanned = deg < (unsigned long long)C0 ? deg : (unsigned long long)C0;
+          // Continue in chunks of 8: all loads of a chunk in flight together.
+          for (OffT e0 = beg[q] + C0; !hit && e0 < end[q]; e0 += 8) {
+            uint32_t x[8], fx[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = __ldcs(&p.col[e0 + c < end[q] ? e0 + c : e0]);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) fx[c] = front[x[c] >> 5];
+            unsigned hm = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              hm |= (unsigned)(e0 + c < end[q] && ((fx[c] >> (x[c] & 31)) & 1u)) << c;
+            }
+            if (hm) {
+              hit = true;
+              scanned += (unsigned long long)__ffs(hm);
+            } else {
+              const OffT rem = end[q] - e0;
+              scanned += rem < 8 ? (unsigned long long)rem : 8ull;
+            }
+          }
         }
         t.edges += scanned;
         if (hit) {
           p.dist[v[q]] = nd;
           atomicOr(&found[(v[q] >> 5) - g * kGroupWords], 1u << (v[q] & 31));
           ++t.produced;
-          if (p.policy == kPolicyBeamer) t.degree += (unsigned long long)(end[q] - beg[q]);
+          if (p.policy == kPolicyBeamer) t.degree += deg;
         }
       }
     }
@@ -628,47 +647,6 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
     if (t.viol) atomicAdd(&cnt->violations, t.viol);
   }
   t = WarpTally{};
-}
-
-// After a bitmap-mode top-down level: visited |= frontier, dist = d+1 for
-// every new vertex (warp-transposed so each store instruction covers one
-// 128 B run of dist), distinct count into cnt->conv_count, Beamer degree sum,
-// and the stale bitmap zeroed (restores the bm[fcur ^ 1] == 0 invariant).
-template <typename OffT>
-__device__ __forceinline__ void merge_frontier(const Params<OffT>& p, const uint32_t* fb,
-                                               uint32_t* stale, uint32_t nd, LevelCnt* cnt) {
-  const unsigned FULL = 0xffffffffu;
-  const unsigned lane = lane_id();
-  const unsigned warps_total = gridDim.x * kWarps;
-  const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  unsigned long long count = 0, degsum = 0;
-  for (uint32_t base = gw * 32; base < p.words; base += warps_total * 32) {
-    const uint32_t w = base + lane;
-    const uint32_t word = fb[w];
-    stale[w] = 0;
-    if (word) p.visited[w] |= word;
-    count += __popc(word);
-    unsigned nz = __ballot_sync(FULL, word != 0);
-    while (nz) {
-      const int j = __ffs(nz) - 1;
-      nz &= nz - 1;
-      const uint32_t wj = __shfl_sync(FULL, word, j);
-      const uint32_t v = (base + j) * 32 + lane;
-      if ((wj >> lane) & 1u) {
-        p.dist[v] = nd;
-        if (p.policy == kPolicyBeamer) degsum += degree_of(p, v);
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    count += __shfl_xor_sync(FULL, count, o);
-    degsum += __shfl_xor_sync(FULL, degsum, o);
-  }
-  if (lane == 0) {
-    if (count) atomicAdd(&cnt->conv_count, (unsigned int)count);
-    if (degsum) atomicAdd(&cnt->degree, degsum);
-  }
 }
 
 // Bitmap -> queue (count_bitmap_slice / write_dense_slice, kernels.cpp:
@@ -770,10 +748,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
   unsigned long long t_start = leader ? globaltimer() : 0;
   bar.sync();
 
-  // Bitmap bookkeeping. bm[fcur] holds the latest frontier whenever it is in
-  // bitmap form; invariant: bm[fcur ^ 1] is all-zero whenever a top-down
-  // level starts (it is the output of a bitmap-mode top-down level and the
-  // mark target when a queue-mode level hands over to bottom-up).
+  // Bitmap bookkeeping (kClaimBitmap). bm[fcur] holds the latest frontier in
+  // bitmap form; invariant: bm[fcur ^ 1] is all-zero when a top-down level
+  // starts. A top-down level marks its winners into bm[fcur ^ 1] and zeroes
+  // the words of its own input frontier in bm[fcur]; then fcur flips.
   uint32_t depth = 0;
   for (;; ++depth) {
     LevelCnt* cnt = &ctl->cnt[depth & 3];
@@ -782,16 +760,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       ctl->cnt[(depth + 2) & 3] = z;
     }
     WarpTally t;
-    // Large top-down frontiers take the bitmap-output path (C == kClaimBitmap).
-    const bool bm_mode = C == kClaimBitmap && td && qlen >= kBitmapMinFrontier;
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
-      uint32_t* obm = bm_mode ? p.bm[fcur ^ 1] : nullptr;
-      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, obm);
+      uint32_t* mark = C == kClaimBitmap ? p.bm[fcur ^ 1] : nullptr;
+      uint32_t* stale = C == kClaimBitmap ? p.bm[fcur] : nullptr;
+      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, stale);
       if (p.max_degree > kHeavyDeg) {
         bar.sync();
         const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
-        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, obm);
+        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, mark);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
@@ -804,20 +781,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true);
       bar.sync();
     }
-    if (bm_mode) {
-      // Merge: visited |= new frontier, distances in vertex order, distinct
-      // count (and Beamer degree sum); clears the stale bitmap.
-      merge_frontier(p, p.bm[fcur ^ 1], p.bm[fcur], depth + 1, cnt);
-      bar.sync();
-      fcur ^= 1;
-    }
+    if (C == kClaimBitmap || !td) fcur ^= 1;  // this level's bitmap is the latest
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
     const unsigned long long produced =
-        (C == kClaimPlain || bm_mode) ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
-                                      : *(volatile unsigned long long*)&cnt->produced;
-    const unsigned long long raw =
-        (td && !bm_mode) ? *(volatile unsigned long long*)&cnt->raw : produced;
+        C == kClaimPlain ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
+                         : *(volatile unsigned long long*)&cnt->produced;
+    const unsigned long long raw = td ? *(volatile unsigned long long*)&cnt->raw : produced;
     const unsigned long long edges = *(volatile unsigned long long*)&cnt->edges;
     const unsigned long long pdeg = *(volatile unsigned long long*)&cnt->degree;
     const unsigned int overflow = *(volatile unsigned int*)&ctl->overflow;
@@ -845,30 +815,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     unvisited_edges -= pdeg;
     const unsigned long long consumed = cur_distinct;
     const bool next_td = decide(td, produced, pdeg, consumed, unvisited_edges);
-    if (!td) fcur ^= 1;  // bottom-up output becomes the latest frontier
     if (td && next_td) {
-      if (bm_mode) {
-        compact_bitmap(p.bm[fcur], p.queue[qcur ^ 1], p.words, &cnt->mark_cursor, false);
-        bar.sync();
-        qlen = *(volatile unsigned int*)&cnt->mark_cursor;
-      } else {
-        qlen = C == kClaimPlain ? produced : raw;
-      }
+      qlen = C == kClaimPlain ? produced : raw;
       qcur ^= 1;
-    } else if (td && !next_td) {
-      if (!bm_mode) {
-        // Entering bottom-up from a queue (mark_bitmap_from_dense,
-        // kernels.cpp:243-260) into bm[fcur ^ 1], zero by the invariant.
-        uint32_t* fb = p.bm[fcur ^ 1];
-        const uint32_t* q = p.queue[qcur ^ 1];
-        for (unsigned long long i = tid; i < raw; i += nthreads) {
-          const uint32_t v = q[i];
-          atomicOr(&fb[v >> 5], 1u << (v & 31));
-        }
-        bar.sync();
-        fcur ^= 1;
-      }
-      // bitmap mode: bm[fcur] already is the frontier, visited is merged.
     } else if (!td && next_td) {
       // Entering top-down: ascending queue from the produced bitmap
       // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241); the
@@ -878,6 +827,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       bar.sync();
       qlen = *(volatile unsigned int*)&cnt->conv_count;
     }
+    // top-down -> bottom-up: bm[fcur] already holds the marked frontier;
+    // bottom-up -> bottom-up: nothing to convert.
     td = next_td;
     cur_raw = raw;
     cur_distinct = produced;
