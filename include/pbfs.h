@@ -243,6 +243,65 @@ pbfs_status pbfs_pick_sources(const pbfs_csr* csr, uint32_t count, uint64_t seed
 pbfs_status pbfs_save_csr1(const pbfs_csr* csr, const char* path);
 pbfs_status pbfs_load_csr1(const char* path, pbfs_host_csr** out);
 
+/* ---- 1D vertex-partitioned multi-GPU BFS (new) ------------
+ * One partition per rank/GPU built on the device from a resident full graph:
+ * hashed relabel pi, row slice (bottom-up) + column slice (top-down). Per
+ * level: pbfs_part_step (local work, writes this rank's slice of `next`),
+ * then the caller allgathers the slices of `next` in place (e.g. NCCL
+ * all_gather with sendbuff = next + rank * words_local), then
+ * pbfs_part_end_level (identical distinct count / direction / termination
+ * on every rank). Partitions on one device may share `frontier`/`next`
+ * (loopback: the allgather is then a no-op). Hybrid (5 % rule) only. */
+typedef struct pbfs_part pbfs_part;
+
+typedef struct pbfs_part_options {
+  uint32_t rank;
+  uint32_t world;
+  uint32_t relabel;        /* 1: hashed pi when n is a power of two */
+  uint32_t reserved;
+  void* shared_frontier;   /* loopback: words_total u32 on the same device, or NULL */
+  void* shared_next;
+} pbfs_part_options;
+
+typedef struct pbfs_part_info {
+  uint64_t vertex_count;
+  uint64_t padded_count;   /* pi-id space (power of two or multiple of 512*world) */
+  uint64_t local_first;    /* first owned pi-id */
+  uint64_t local_count;    /* owned pi-ids */
+  uint64_t local_arcs;     /* row-slice arcs (= column-slice arcs) */
+  uint64_t words_total;    /* full bitmap words */
+  uint64_t words_local;    /* this rank's slice: next + rank * words_local */
+  uint32_t rank;
+  uint32_t world;
+  uint32_t relabel_hashed;
+  uint32_t depth;
+  uint32_t top_down;
+  uint32_t reserved;
+  uint32_t* frontier;      /* device, current frontier bitmap (full) */
+  uint32_t* next;          /* device, next frontier bitmap (full; allgather target) */
+  uint32_t* dist_local;    /* device, local_count entries, pi-space */
+} pbfs_part_info;
+
+/* Device pointers of a resident graph (for building partitions). */
+pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offsets,
+                                     const uint32_t** column_indices, uint32_t* offset_bytes);
+pbfs_status pbfs_part_create(const pbfs_graph* full, const pbfs_part_options* opt,
+                             pbfs_part** out);
+pbfs_status pbfs_part_destroy(pbfs_part* p);
+pbfs_status pbfs_part_get_info(const pbfs_part* p, pbfs_part_info* info);
+pbfs_status pbfs_part_relabel(const pbfs_part* p, uint64_t v, uint64_t* pi_v);
+pbfs_status pbfs_part_begin(pbfs_part* p, uint32_t source, const pbfs_config* cfg, void* stream);
+pbfs_status pbfs_part_step(pbfs_part* p, void* stream);
+pbfs_status pbfs_part_end_level(pbfs_part* p, void* stream, uint32_t* done, pbfs_level* rec);
+pbfs_status pbfs_part_sync(pbfs_part* p, void* stream);
+/* dist[v] = dist_pi[pi(v)] for v < vertex_count (dist_pi: padded_count entries,
+ * the ranks' dist_local slices concatenated). */
+pbfs_status pbfs_part_unrelabel(pbfs_part* p, const uint32_t* dist_pi, uint32_t* dist, void* stream);
+/* Host-side helpers: copy this rank's dist_local (local_count u32) to host;
+ * un-relabel a host pi-space array (padded_count entries) into dist (n). */
+pbfs_status pbfs_part_copy_dist(pbfs_part* p, uint32_t* host_out);
+pbfs_status pbfs_part_unrelabel_host(const pbfs_part* p, const uint32_t* dist_pi, uint32_t* dist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,19 @@ class Stats(ctypes.Structure):
                 ("max_degree", c_u64), ("large_diameter", c_u32), ("reserved", c_u32)]
 
 
+class PartOptions(ctypes.Structure):
+    _fields_ = [("rank", c_u32), ("world", c_u32), ("relabel", c_u32), ("reserved", c_u32),
+                ("shared_frontier", c_vp), ("shared_next", c_vp)]
+
+
+class PartInfo(ctypes.Structure):
+    _fields_ = [("vertex_count", c_u64), ("padded_count", c_u64), ("local_first", c_u64),
+                ("local_count", c_u64), ("local_arcs", c_u64), ("words_total", c_u64),
+                ("words_local", c_u64), ("rank", c_u32), ("world", c_u32),
+                ("relabel_hashed", c_u32), ("depth", c_u32), ("top_down", c_u32),
+                ("reserved", c_u32), ("frontier", c_vp), ("next", c_vp), ("dist_local", c_vp)]
+
+
 P = ctypes.POINTER
 
 # (name, restype, argtypes) for every symbol include/pbfs.h declares.
@@ -96,6 +109,18 @@ SIGNATURES = [
     ("pbfs_pick_sources", ctypes.c_int, [P(Csr), c_u32, c_u64, c_vp]),
     ("pbfs_save_csr1", ctypes.c_int, [P(Csr), ctypes.c_char_p]),
     ("pbfs_load_csr1", ctypes.c_int, [ctypes.c_char_p, P(c_vp)]),
+    ("pbfs_graph_device_arrays", ctypes.c_int, [c_vp, P(c_vp), P(c_vp), P(c_u32)]),
+    ("pbfs_part_create", ctypes.c_int, [c_vp, P(PartOptions), P(c_vp)]),
+    ("pbfs_part_destroy", ctypes.c_int, [c_vp]),
+    ("pbfs_part_get_info", ctypes.c_int, [c_vp, P(PartInfo)]),
+    ("pbfs_part_relabel", ctypes.c_int, [c_vp, c_u64, P(c_u64)]),
+    ("pbfs_part_begin", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),
+    ("pbfs_part_step", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_part_end_level", ctypes.c_int, [c_vp, c_vp, P(c_u32), P(Level)]),
+    ("pbfs_part_sync", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_part_unrelabel", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    ("pbfs_part_copy_dist", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_part_unrelabel_host", ctypes.c_int, [c_vp, c_vp, c_vp]),
 ]
 
 

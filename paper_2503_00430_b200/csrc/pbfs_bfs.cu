@@ -539,6 +539,17 @@ pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream) {
   return PBFS_OK;
 }
 
+pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offsets,
+                                     const uint32_t** column_indices, uint32_t* offset_bytes) {
+  if (!g || !row_offsets || !column_indices || !offset_bytes) {
+    return fail(PBFS_E_INPUT, "null argument");
+  }
+  *row_offsets = g->rowptr;
+  *column_indices = g->col;
+  *offset_bytes = g->offb;
+  return PBFS_OK;
+}
+
 pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev) {
   if (!g || !dist_dev) return fail(PBFS_E_INPUT, "null argument");
   *dist_dev = g->dist;

@@ -1,0 +1,680 @@
+// 1D vertex-partitioned BFS: one partition per GPU, one
+// frontier-bitmap allgather per level.
+//
+//   * Vertices are relabelled by a bijective hash pi on [0, 2^k) (multiply by
+//     an odd constant, xor-shift, multiply again; identity + padding when n is
+//     not a power of two) so every rank owns an equal share of the RMAT arcs
+//     (unpermuted RMAT puts ~42 % of arcs on one of 8 contiguous ranks).
+//   * Rank r owns pi-ids [r*nloc, (r+1)*nloc) and stores
+//       - the ROW slice: full adjacency of its owned vertices (neighbours as
+//         global pi-ids) -- bottom-up scans it against the replicated frontier;
+//       - the COLUMN slice: for every global pi-id u, u's owned neighbours as
+//         local ids (the transpose of the row slice; the graph is symmetric)
+//         -- top-down expands the whole replicated frontier over it.
+//     Either way discoveries are owner-local: dist / visited stores stay
+//     local and the claim atomics never cross a GPU.
+//   * After each level every rank holds only its own slice of the next
+//     frontier bitmap; the host exchanges slices with one allgather (NCCL
+//     over NVLink, in place) and every rank then derives the identical
+//     distinct count, direction and termination from the full bitmap.
+//
+// The per-rank level code is the single-GPU engine's device code
+// (pbfs_kernels.cuh: td_phase_light / td_phase_heavy / bu_phase /
+// compact_bitmap) run over partition-shaped Params, one launch per phase.
+// Partitions on the SAME device may share the full bitmaps ("loopback"),
+// which turns the allgather into a no-op; tests use it to check G-way
+// partitioned traversals bit-exactly on one B200.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "pbfs_internal.h"
+#include "pbfs_kernels.cuh"
+
+using namespace pbfs;
+using namespace pbfs::dev;
+
+
+namespace {
+
+// ---- relabel pi on [0, 2^k) ---------------------------------------------------
+struct Relabel {
+  uint32_t k = 0;       // n_pad = 2^k when hashed
+  uint32_t hashed = 0;  // 0: identity
+  uint64_t mask = 0;
+  uint64_t a = 0, ainv = 0, b = 0, binv = 0;
+  uint32_t h = 0;
+};
+
+uint64_t inv_odd(uint64_t a, uint64_t mask) {  // a^-1 mod 2^k (Newton)
+  uint64_t x = a;
+  for (int i = 0; i < 6; ++i) x *= 2 - a * x;
+  return x & mask;
+}
+
+Relabel make_relabel(uint32_t k, bool hashed) {
+  Relabel r;
+  r.k = k;
+  r.hashed = hashed && k >= 2;
+  r.mask = k >= 64 ? ~0ull : ((1ull << k) - 1);
+  r.a = 0x9E3779B97F4A7C15ull & r.mask;
+  r.b = 0xC2B2AE3D27D4EB4Full & r.mask;
+  r.a |= 1;
+  r.b |= 1;
+  r.ainv = inv_odd(r.a, r.mask);
+  r.binv = inv_odd(r.b, r.mask);
+  r.h = (k + 1) / 2;  // 2h >= k: x ^= x >> h is its own inverse
+  return r;
+}
+
+__host__ __device__ __forceinline__ uint64_t pi_fwd(const Relabel& r, uint64_t v) {
+  if (!r.hashed) return v;
+  uint64_t x = (v * r.a) & r.mask;
+  x ^= x >> r.h;
+  return (x * r.b) & r.mask;
+}
+__host__ __device__ __forceinline__ uint64_t pi_inv(const Relabel& r, uint64_t y) {
+  if (!r.hashed) return y;
+  uint64_t x = (y * r.binv) & r.mask;
+  x ^= x >> r.h;
+  return (x * r.ainv) & r.mask;
+}
+
+// ---- partition-build kernels ---------------------------------------------------
+template <typename OffT>
+__global__ void k_local_degrees(const OffT* __restrict__ rowptr, uint64_t n, Relabel rl,
+                                uint64_t lo, uint64_t nloc, unsigned long long* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = pi_inv(rl, lo + i);
+    deg[i] = v < n ? (unsigned long long)(rowptr[v + 1] - rowptr[v]) : 0ull;
+  }
+}
+
+// Warp per owned vertex: relabelled neighbour list into the row slice, and
+// a count of each neighbour for the column slice.
+template <typename OffT>
+__global__ void k_fill_rows(const OffT* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                            uint64_t n, Relabel rl, uint64_t lo, uint64_t nloc,
+                            const unsigned long long* __restrict__ rowloc, uint32_t* colrow,
+                            unsigned long long* colcnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; i < nloc;
+       i += warps) {
+    const uint64_t v = pi_inv(rl, lo + i);
+    if (v >= n) continue;
+    const uint64_t b = rowptr[v], e = rowptr[v + 1], out = rowloc[i];
+    for (uint64_t k = b + lane; k < e; k += 32) {
+      const uint32_t u = (uint32_t)pi_fwd(rl, col[k]);
+      colrow[out + (k - b)] = u;
+      atomicAdd(&colcnt[u], 1ull);
+    }
+  }
+}
+
+__global__ void k_fill_cols(const unsigned long long* __restrict__ rowloc,
+                            const uint32_t* __restrict__ colrow, uint64_t nloc,
+                            unsigned long long* cursor, uint32_t* colcol) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; i < nloc;
+       i += warps) {
+    for (uint64_t k = rowloc[i] + lane; k < rowloc[i + 1]; k += 32) {
+      const uint32_t u = colrow[k];
+      const unsigned long long pos = atomicAdd(&cursor[u], 1ull);
+      colcol[pos] = (uint32_t)i;
+    }
+  }
+}
+
+__global__ void k_col_stats(const unsigned long long* __restrict__ colptr, uint64_t npad,
+                            unsigned long long* maxdeg, unsigned long long* heavy_items) {
+  unsigned long long mx = 0, hv = 0;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < npad;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = colptr[u + 1] - colptr[u];
+    mx = d > mx ? d : mx;
+    if (d > kHeavyDeg) hv += (d + kChunk - 1) / kChunk;
+  }
+  atomicMax(maxdeg, mx);
+  if (hv) atomicAdd(heavy_items, hv);
+}
+
+__global__ void k_local_mask(const unsigned long long* __restrict__ rowloc, uint64_t nloc,
+                             uint64_t words, uint32_t* mask) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    for (int b = 0; b < 32; ++b) {
+      const uint64_t i = w * 32 + b;
+      if (i >= nloc || rowloc[i + 1] == rowloc[i]) m |= 1u << b;  // isolated / padding
+    }
+    mask[w] = m;
+  }
+}
+
+// ---- per-level kernels -------------------------------------------------------------
+struct PartState {
+  unsigned long long qlen;
+  unsigned long long distinct;
+};
+
+__global__ void k_begin(uint32_t* dist, uint32_t* visited, const uint32_t* mask, uint64_t nloc,
+                        uint64_t lwords, uint32_t* front, uint32_t* next, uint64_t clear_lo,
+                        uint64_t clear_words, uint64_t src_pi, uint64_t lo, bool set_src_bit,
+                        uint32_t* queue, PartState* st) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const bool owner = src_pi >= lo && src_pi < lo + nloc;
+  for (uint64_t i = tid; i < nloc; i += nth) dist[i] = (owner && i == src_pi - lo) ? 0u : kUnreached;
+  for (uint64_t w = tid; w < lwords; w += nth) {
+    uint32_t m = mask[w];
+    if (owner && w == (src_pi - lo) / 32) m |= 1u << ((src_pi - lo) & 31);
+    visited[w] = m;
+  }
+  for (uint64_t w = tid; w < clear_words; w += nth) {
+    const uint64_t gw = clear_lo + w;
+    front[gw] = (set_src_bit && gw == src_pi / 32) ? (1u << (src_pi & 31)) : 0u;
+    next[gw] = 0u;
+  }
+  if (tid == 0) {
+    queue[0] = (uint32_t)src_pi;
+    st->qlen = 1;
+    st->distinct = 1;
+  }
+}
+
+__global__ void k_clear(uint32_t* p, uint64_t words) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    p[w] = 0u;
+  }
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kThreads) k_td_light(Params<OffT> p, uint32_t depth,
+                                                       const uint32_t* qin, const PartState* st,
+                                                       uint32_t* qout, uint32_t* mark) {
+  __shared__ uint32_t s_buf[kWarps][kPushBuf];
+  WarpPush wp{s_buf[threadIdx.x >> 5], 0};
+  WarpTally t;
+  LevelCnt* cnt = &p.ctl->cnt[0];
+  td_phase_light<kClaimBitmap>(p, depth, qin, st->qlen, qout, wp, cnt, t, mark, nullptr);
+  wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  warp_flush_tally(cnt, t, false);
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kThreads) k_td_heavy(Params<OffT> p, uint32_t depth,
+                                                       uint32_t* qout, uint32_t* mark) {
+  __shared__ uint32_t s_buf[kWarps][kPushBuf];
+  WarpPush wp{s_buf[threadIdx.x >> 5], 0};
+  WarpTally t;
+  LevelCnt* cnt = &p.ctl->cnt[0];
+  const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
+  if (items) td_phase_heavy<kClaimBitmap>(p, depth, items, qout, wp, cnt, t, mark);
+  wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  warp_flush_tally(cnt, t, false);
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kThreads) k_bu(Params<OffT> p, uint32_t depth,
+                                                 const uint32_t* front, uint32_t* next_local) {
+  __shared__ uint32_t s_list[kWarps][kGroupVerts];
+  __shared__ uint32_t s_found[kWarps][kGroupWords];
+  const unsigned warp = threadIdx.x >> 5;
+  WarpTally t;
+  bu_phase(p, depth, front, next_local, s_list[warp], s_found[warp], t);
+  warp_flush_tally(&p.ctl->cnt[0], t, false);
+}
+
+__global__ void k_popcount(const uint32_t* __restrict__ bm, uint64_t words, PartState* st) {
+  unsigned long long c = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    c += __popc(bm[w]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&st->distinct, c);
+}
+
+__global__ void k_compact(uint32_t* bm, uint64_t words, uint32_t* queue, LevelCnt* cnt,
+                          PartState* st) {
+  compact_bitmap(bm, queue, (uint32_t)words, &cnt->conv_count, false);
+}
+
+__global__ void k_set_qlen(const LevelCnt* cnt, PartState* st) {
+  st->qlen = cnt->conv_count;
+}
+
+__global__ void k_unrelabel(const uint32_t* __restrict__ dist_pi, uint64_t n, Relabel rl,
+                            uint32_t* dist) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    dist[v] = dist_pi[pi_fwd(rl, v)];
+  }
+}
+
+}  // namespace
+
+struct pbfs_part {
+  int device = 0;
+  uint32_t rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  Relabel rl;
+  uint64_t n = 0, npad = 0, nloc = 0, lo = 0;
+  uint64_t words_total = 0, lwords = 0;
+  uint64_t m_loc = 0;
+  uint32_t offb = 8;
+  bool shared = false;
+  int grid = 0;
+  // row slice (bottom-up)
+  unsigned long long* rowloc = nullptr;  // nloc + 1
+  uint32_t* colrow = nullptr;            // m_loc, global pi-ids
+  // column slice (top-down)
+  unsigned long long* colptr = nullptr;  // npad + 1
+  uint32_t* colcol = nullptr;            // m_loc, local ids
+  uint64_t col_maxdeg = 0, heavy_cap = 0;
+  // traversal state
+  uint32_t* dist = nullptr;      // nloc
+  uint32_t* visited = nullptr;   // lwords
+  uint32_t* mask = nullptr;      // lwords
+  uint32_t* bm[2] = {nullptr, nullptr};  // full bitmaps (own or shared)
+  int fcur = 0;                  // bm[fcur] = current frontier, bm[fcur^1] = next
+  uint32_t* queue[2] = {nullptr, nullptr};
+  int qcur = 0;
+  HeavyItem* heavy = nullptr;
+  Ctl* ctl = nullptr;
+  PartState* st = nullptr;
+  PartState* st_host = nullptr;  // pinned mirror
+  std::vector<void*> allocs;
+  // level state (identical on every rank)
+  uint32_t depth = 0;
+  bool td = true;
+  int policy = kPolicyFraction;
+  double threshold = 0.05;
+  unsigned long long cur_distinct = 1;
+  unsigned long long edges_level = 0;
+};
+
+namespace {
+
+pbfs_status cuda_fail_p(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  return fail(PBFS_E_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define PCUDA(call, what)                                   \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess) return cuda_fail_p(_e, what);    \
+  } while (0)
+
+template <typename T>
+pbfs_status palloc(pbfs_part* g, T** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PBFS_E_CAPACITY, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  g->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return PBFS_OK;
+}
+
+void part_release(pbfs_part* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  for (void* p : g->allocs) cudaFree(p);
+  if (g->st_host) cudaFreeHost(g->st_host);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+Params<unsigned long long> td_params(const pbfs_part* g) {
+  Params<unsigned long long> p{};
+  p.rowptr = g->colptr;
+  p.col = g->colcol;
+  p.dist = g->dist;
+  p.visited = g->visited;
+  p.heavy = g->heavy;
+  p.ctl = g->ctl;
+  p.qcap = g->nloc + 1;
+  p.heavy_cap = g->heavy_cap;
+  p.n = g->nloc;
+  p.words = (uint32_t)g->lwords;
+  p.policy = g->policy;
+  p.threshold = g->threshold;
+  return p;
+}
+
+Params<unsigned long long> bu_params(const pbfs_part* g) {
+  Params<unsigned long long> p{};
+  p.rowptr = g->rowloc;
+  p.col = g->colrow;
+  p.dist = g->dist;
+  p.visited = g->visited;
+  p.ctl = g->ctl;
+  p.n = g->nloc;
+  p.words = (uint32_t)g->lwords;
+  p.policy = g->policy;
+  p.threshold = g->threshold;
+  return p;
+}
+
+template <typename OffT>
+pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* col) {
+  cudaStream_t s = g->stream;
+  const int blocks = g->grid;
+  unsigned long long* deg = nullptr;
+  pbfs_status st;
+  if ((st = palloc(g, &g->rowloc, (g->nloc + 1) * 8)) != PBFS_OK) return st;
+  if ((st = palloc(g, &deg, (g->nloc + 1) * 8)) != PBFS_OK) return st;
+  PCUDA(cudaMemsetAsync(deg, 0, (g->nloc + 1) * 8, s), "memset");
+  k_local_degrees<OffT><<<blocks, 256, 0, s>>>(rowptr, g->n, g->rl, g->lo, g->nloc, deg);
+  // rowloc = exclusive scan of deg (nloc + 1 entries; deg[nloc] = 0)
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg, g->rowloc, (int64_t)(g->nloc + 1), s);
+  size_t tmp2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, deg, g->rowloc, (int64_t)(g->npad + 1), s);
+  tmp_bytes = std::max(tmp_bytes, tmp2);
+  void* tmp = nullptr;
+  PCUDA(cudaMalloc(&tmp, tmp_bytes), "scan scratch");
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, g->rowloc, (int64_t)(g->nloc + 1), s);
+  unsigned long long mloc = 0;
+  PCUDA(cudaMemcpyAsync(&mloc, g->rowloc + g->nloc, 8, cudaMemcpyDeviceToHost, s), "read m_loc");
+  PCUDA(cudaStreamSynchronize(s), "partition scan");
+  g->m_loc = mloc;
+  unsigned long long* colcnt = nullptr;
+  if ((st = palloc(g, &g->colrow, (g->m_loc + 8) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  if ((st = palloc(g, &colcnt, (g->npad + 1) * 8)) != PBFS_OK) { cudaFree(tmp); return st; }
+  PCUDA(cudaMemsetAsync(colcnt, 0, (g->npad + 1) * 8, s), "memset");
+  k_fill_rows<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->rl, g->lo, g->nloc, g->rowloc,
+                                           g->colrow, colcnt);
+  if ((st = palloc(g, &g->colptr, (g->npad + 1) * 8)) != PBFS_OK) { cudaFree(tmp); return st; }
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, colcnt, g->colptr, (int64_t)(g->npad + 1), s);
+  if ((st = palloc(g, &g->colcol, (g->m_loc + 8) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  // cursor = colptr copy (reuse colcnt)
+  PCUDA(cudaMemcpyAsync(colcnt, g->colptr, (g->npad + 1) * 8, cudaMemcpyDeviceToDevice, s), "copy");
+  k_fill_cols<<<blocks, 256, 0, s>>>(g->rowloc, g->colrow, g->nloc, colcnt, g->colcol);
+  unsigned long long* stats = deg;  // reuse: [0] maxdeg, [1] heavy items
+  PCUDA(cudaMemsetAsync(stats, 0, 16, s), "memset");
+  k_col_stats<<<blocks, 256, 0, s>>>(g->colptr, g->npad, stats, stats + 1);
+  unsigned long long hs[2];
+  PCUDA(cudaMemcpyAsync(hs, stats, 16, cudaMemcpyDeviceToHost, s), "read stats");
+  if ((st = palloc(g, &g->mask, g->lwords * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  k_local_mask<<<blocks, 256, 0, s>>>(g->rowloc, g->nloc, g->lwords, g->mask);
+  PCUDA(cudaGetLastError(), "partition kernels");
+  PCUDA(cudaStreamSynchronize(s), "partition build");
+  cudaFree(tmp);
+  g->col_maxdeg = hs[0];
+  g->heavy_cap = hs[1];
+  return PBFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pbfs_status pbfs_part_create(const pbfs_graph* full, const pbfs_part_options* opt,
+                             pbfs_part** out) {
+  if (!full || !opt || !out) return fail(PBFS_E_INPUT, "null argument");
+  if (opt->world < 1 || opt->rank >= opt->world) return fail(PBFS_E_CONFIG, "bad rank/world");
+  pbfs_graph_info gi;
+  pbfs_status st = pbfs_graph_get_info(full, &gi);
+  if (st != PBFS_OK) return st;
+  if (!gi.symmetric) {
+    return fail(PBFS_E_INPUT, "the vertex partition needs a symmetric graph (its column "
+                              "slice is the transpose of the row slice)");
+  }
+  const void* rowptr = nullptr;
+  const uint32_t* col = nullptr;
+  uint32_t offb = 0;
+  if ((st = pbfs_graph_device_arrays(full, &rowptr, &col, &offb)) != PBFS_OK) return st;
+
+  auto* g = new (std::nothrow) pbfs_part;
+  if (!g) return fail(PBFS_E_CAPACITY, "host allocation failed");
+  g->device = gi.device;
+  g->rank = opt->rank;
+  g->world = opt->world;
+  g->n = gi.vertex_count;
+  g->offb = offb;
+  // Padded id space: a power of two (hashed relabel) or the next multiple of
+  // 512 * world (identity), so every rank's slice is whole 16-word groups.
+  uint32_t k = 0;
+  while ((1ull << k) < g->n) ++k;
+  const bool pow2 = (1ull << k) == g->n;
+  const uint64_t quantum = 512ull * g->world;
+  if (pow2 && opt->relabel && g->n >= quantum) {
+    g->npad = g->n;
+    g->rl = make_relabel(k, true);
+  } else {
+    g->npad = (g->n + quantum - 1) / quantum * quantum;
+    g->rl = make_relabel(k, false);
+  }
+  g->nloc = g->npad / g->world;
+  g->lo = g->nloc * g->rank;
+  g->words_total = g->npad / 32;
+  g->lwords = g->nloc / 32;
+  g->shared = opt->shared_frontier && opt->shared_next;
+  cudaSetDevice(g->device);
+  auto bail = [&](pbfs_status s2) {
+    part_release(g);
+    return s2;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail(cuda_fail_p(e, "stream"));
+  int occ = 0;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, g->device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_td_light<unsigned long long>, kThreads, 0);
+  g->grid = prop.multiProcessorCount * std::max(occ, 1);
+  st = offb == 8 ? build_partition<unsigned long long>(g, static_cast<const unsigned long long*>(rowptr), col)
+                 : build_partition<uint32_t>(g, static_cast<const uint32_t*>(rowptr), col);
+  if (st != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->dist, g->nloc * 4 + 16)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->visited, g->lwords * 4)) != PBFS_OK) return bail(st);
+  if (g->shared) {
+    g->bm[0] = static_cast<uint32_t*>(opt->shared_frontier);
+    g->bm[1] = static_cast<uint32_t*>(opt->shared_next);
+  } else {
+    if ((st = palloc(g, &g->bm[0], g->words_total * 4)) != PBFS_OK) return bail(st);
+    if ((st = palloc(g, &g->bm[1], g->words_total * 4)) != PBFS_OK) return bail(st);
+  }
+  if ((st = palloc(g, &g->queue[0], (g->npad + 1) * 4)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->queue[1], (g->npad + 1) * 4)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->heavy, std::max<uint64_t>(g->heavy_cap, 1) * sizeof(HeavyItem))) != PBFS_OK)
+    return bail(st);
+  if ((st = palloc(g, &g->ctl, sizeof(Ctl))) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->st, sizeof(PartState))) != PBFS_OK) return bail(st);
+  if ((e = cudaMallocHost(&g->st_host, sizeof(PartState))) != cudaSuccess)
+    return bail(cuda_fail_p(e, "pinned state"));
+  PCUDA(cudaMemset(g->ctl, 0, sizeof(Ctl)), "memset");
+  *out = g;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_destroy(pbfs_part* g) {
+  part_release(g);
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_get_info(const pbfs_part* g, pbfs_part_info* info) {
+  if (!g || !info) return fail(PBFS_E_INPUT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->vertex_count = g->n;
+  info->padded_count = g->npad;
+  info->local_first = g->lo;
+  info->local_count = g->nloc;
+  info->local_arcs = g->m_loc;
+  info->words_total = g->words_total;
+  info->words_local = g->lwords;
+  info->rank = g->rank;
+  info->world = g->world;
+  info->relabel_hashed = g->rl.hashed;
+  info->frontier = g->bm[g->fcur];
+  info->next = g->bm[g->fcur ^ 1];
+  info->dist_local = g->dist;
+  info->depth = g->depth;
+  info->top_down = g->td ? 1u : 0u;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_relabel(const pbfs_part* g, uint64_t v, uint64_t* pi_v) {
+  if (!g || !pi_v) return fail(PBFS_E_INPUT, "null argument");
+  if (v >= g->n) return fail(PBFS_E_INPUT, "vertex out of range");
+  *pi_v = pi_fwd(g->rl, v);
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_begin(pbfs_part* g, uint32_t source, const pbfs_config* cfg, void* stream) {
+  if (!g || !cfg) return fail(PBFS_E_INPUT, "null argument");
+  pbfs_status st = pbfs_config_validate(cfg);
+  if (st != PBFS_OK) return st;
+  if (cfg->variant != PBFS_HYBRID && cfg->variant != PBFS_VISITED_INLINE) {
+    return fail(PBFS_E_CONFIG, "the partitioned engine runs the hybrid (5 % rule) traversal");
+  }
+  if (source >= g->n) {
+    return fail(PBFS_E_INPUT, "source vertex " + std::to_string(source) +
+                                  " is out of range for a graph with " + std::to_string(g->n) +
+                                  " vertices");
+  }
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  g->policy = cfg->force_top_down_only ? kPolicyTopDown : kPolicyFraction;
+  g->threshold = cfg->hybrid_threshold_fraction;
+  g->fcur = 0;
+  g->qcur = 0;
+  g->depth = 0;
+  const uint64_t spi = pi_fwd(g->rl, source);
+  const uint64_t clear_lo = g->shared ? g->lo / 32 : 0;
+  const uint64_t clear_words = g->shared ? g->lwords : g->words_total;
+  const bool set_bit = !g->shared || (spi >= g->lo && spi < g->lo + g->nloc);
+  k_begin<<<g->grid, 256, 0, s>>>(g->dist, g->visited, g->mask, g->nloc, g->lwords, g->bm[0],
+                                  g->bm[1], clear_lo, clear_words, spi, g->lo, set_bit,
+                                  g->queue[0], g->st);
+  PCUDA(cudaGetLastError(), "begin");
+  PCUDA(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s), "memset ctl");
+  // decide_direction for the seed (kernels.cpp:154-156); the source degree
+  // is not needed by the size-fraction rule.
+  g->td = g->policy == kPolicyTopDown || 1.0 < g->threshold * (double)g->n;
+  g->cur_distinct = 1;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_step(pbfs_part* g, void* stream) {
+  if (!g) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  PCUDA(cudaMemsetAsync(&g->ctl->cnt[0], 0, sizeof(LevelCnt), s), "memset counters");
+  uint32_t* next = g->bm[g->fcur ^ 1];
+  uint32_t* next_local = next + g->lo / 32;
+  if (g->td) {
+    // Own slice of the next bitmap must be zero before claims mark it.
+    k_clear<<<g->grid, 256, 0, s>>>(next_local, g->lwords);
+    Params<unsigned long long> p = td_params(g);
+    k_td_light<unsigned long long><<<g->grid, kThreads, 0, s>>>(
+        p, g->depth, g->queue[g->qcur], g->st, g->queue[g->qcur ^ 1], next_local);
+    if (g->col_maxdeg > kHeavyDeg) {
+      k_td_heavy<unsigned long long><<<g->grid, kThreads, 0, s>>>(p, g->depth,
+                                                                 g->queue[g->qcur ^ 1], next_local);
+    }
+  } else {
+    Params<unsigned long long> p = bu_params(g);
+    k_bu<unsigned long long><<<g->grid, kThreads, 0, s>>>(p, g->depth, g->bm[g->fcur], next_local);
+  }
+  PCUDA(cudaGetLastError(), "level launch");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_end_level(pbfs_part* g, void* stream, uint32_t* done, pbfs_level* rec) {
+  if (!g || !done) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  uint32_t* next = g->bm[g->fcur ^ 1];
+  // Distinct size of the (allgathered) next frontier: same value on every rank.
+  PCUDA(cudaMemsetAsync(&g->st->distinct, 0, 8, s), "memset");
+  k_popcount<<<g->grid, 256, 0, s>>>(next, g->words_total, g->st);
+  unsigned long long edges = 0;
+  PCUDA(cudaMemcpyAsync(&edges, &g->ctl->cnt[0].edges, 8, cudaMemcpyDeviceToHost, s), "read");
+  PCUDA(cudaMemcpyAsync(g->st_host, g->st, sizeof(PartState), cudaMemcpyDeviceToHost, s), "read");
+  unsigned int overflow = 0;
+  PCUDA(cudaMemcpyAsync(&overflow, &g->ctl->overflow, 4, cudaMemcpyDeviceToHost, s), "read");
+  PCUDA(cudaStreamSynchronize(s), "level");
+  if (overflow) return fail(PBFS_E_CAPACITY, "partition frontier overflow");
+  const unsigned long long produced = g->st_host->distinct;
+  if (rec) {
+    rec->depth = g->depth;
+    rec->phase = g->td ? PBFS_TOP_DOWN : PBFS_BOTTOM_UP;
+    rec->frontier_size = g->cur_distinct;
+    rec->distinct_size = g->cur_distinct;
+    rec->duplicate_count = 0;
+    rec->edges_examined = edges;  // this rank's share
+    rec->flush_events = 0;
+    rec->elapsed_ns = 0;
+  }
+  if (produced == 0) {
+    *done = 1;
+    return PBFS_OK;
+  }
+  *done = 0;
+  const bool next_td = g->policy == kPolicyTopDown ||
+                       (double)produced < g->threshold * (double)g->n;
+  g->fcur ^= 1;  // next becomes the frontier
+  if (next_td) {
+    // Every rank compacts the full frontier (global pi-ids) into its queue.
+    PCUDA(cudaMemsetAsync(&g->ctl->cnt[1], 0, sizeof(LevelCnt), s), "memset");
+    g->qcur = 0;
+    k_compact<<<g->grid, kThreads, 0, s>>>(g->bm[g->fcur], g->words_total, g->queue[0],
+                                           &g->ctl->cnt[1], g->st);
+    k_set_qlen<<<1, 1, 0, s>>>(&g->ctl->cnt[1], g->st);
+    PCUDA(cudaGetLastError(), "compact");
+  }
+  g->td = next_td;
+  g->cur_distinct = produced;
+  ++g->depth;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_unrelabel(pbfs_part* g, const uint32_t* dist_pi, uint32_t* dist,
+                                void* stream) {
+  if (!g || !dist_pi || !dist) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  k_unrelabel<<<g->grid, 256, 0, s>>>(dist_pi, g->n, g->rl, dist);
+  PCUDA(cudaGetLastError(), "unrelabel");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_copy_dist(pbfs_part* g, uint32_t* host_out) {
+  if (!g || !host_out) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PCUDA(cudaStreamSynchronize(g->stream), "sync");
+  PCUDA(cudaMemcpy(host_out, g->dist, g->nloc * 4, cudaMemcpyDeviceToHost), "copy dist");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_unrelabel_host(const pbfs_part* g, const uint32_t* dist_pi, uint32_t* dist) {
+  if (!g || !dist_pi || !dist) return fail(PBFS_E_INPUT, "null argument");
+  for (uint64_t v = 0; v < g->n; ++v) dist[v] = dist_pi[pi_fwd(g->rl, v)];
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_sync(pbfs_part* g, void* stream) {
+  if (!g) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PCUDA(cudaStreamSynchronize(stream ? static_cast<cudaStream_t>(stream) : g->stream), "sync");
+  return PBFS_OK;
+}
+
+}  // extern "C"

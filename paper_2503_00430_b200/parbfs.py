@@ -647,3 +647,107 @@ def time_run(graph: CsrGraph, source: int, config: KernelConfig, trials: int, wa
     order = sorted(range(trials), key=lambda i: samples[i])
     mid = order[(trials - 1) // 2]
     return TimingReport(samples[mid], samples, traces[mid])
+
+
+# ---- 1D vertex-partitioned multi-GPU traversal ------------------------
+class PartitionedGraph:
+    """One rank's partition of a resident graph (pbfs_part handle).
+
+    Per level: ``step()`` (local work), then the caller exchanges the slices
+    of ``info()['next']`` (an in-place allgather of ``words_local`` uint32
+    words per rank, e.g. NCCL over NVLink), then ``end_level()``.
+    """
+
+    def __init__(self, dgraph: DeviceGraph, rank: int, world: int, relabel: bool = True,
+                 shared: Optional["PartitionedGraph"] = None):
+        opt = L.PartOptions()
+        opt.rank, opt.world, opt.relabel = int(rank), int(world), int(bool(relabel))
+        if shared is not None:
+            si = shared.info()
+            opt.shared_frontier, opt.shared_next = si["frontier"], si["next"]
+        h = ctypes.c_void_p()
+        _check(lib.pbfs_part_create(dgraph.h, ctypes.byref(opt), ctypes.byref(h)))
+        self.h = h
+        self._keep = (dgraph, shared)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.pbfs_part_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = L.PartInfo()
+        _check(lib.pbfs_part_get_info(self.h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in L.PartInfo._fields_}
+
+    def begin(self, source: int, config: KernelConfig, stream: int = 0) -> None:
+        c = config._c()
+        _check(lib.pbfs_part_begin(self.h, int(source), ctypes.byref(c),
+                                   ctypes.c_void_p(stream) if stream else None))
+
+    def step(self, stream: int = 0) -> None:
+        _check(lib.pbfs_part_step(self.h, ctypes.c_void_p(stream) if stream else None))
+
+    def end_level(self, stream: int = 0):
+        done = ctypes.c_uint32()
+        rec = L.Level()
+        _check(lib.pbfs_part_end_level(self.h, ctypes.c_void_p(stream) if stream else None,
+                                       ctypes.byref(done), ctypes.byref(rec)))
+        return bool(done.value), LevelRecord(rec.depth, TraversalPhase(rec.phase),
+                                             rec.frontier_size, rec.distinct_size,
+                                             rec.duplicate_count, rec.edges_examined, 0, 0)
+
+    def sync(self, stream: int = 0) -> None:
+        _check(lib.pbfs_part_sync(self.h, ctypes.c_void_p(stream) if stream else None))
+
+    def local_distances(self) -> np.ndarray:
+        out = np.empty(self.info()["local_count"], dtype=np.uint32)
+        _check(lib.pbfs_part_copy_dist(self.h, out.ctypes.data))
+        return out
+
+    def unrelabel_host(self, dist_pi: np.ndarray) -> np.ndarray:
+        dist_pi = np.ascontiguousarray(dist_pi, dtype=np.uint32)
+        out = np.empty(self.info()["vertex_count"], dtype=np.uint32)
+        _check(lib.pbfs_part_unrelabel_host(self.h, dist_pi.ctypes.data, out.ctypes.data))
+        return out
+
+    def unrelabel(self, dist_pi_dev: int, dist_dev: int, stream: int = 0) -> None:
+        _check(lib.pbfs_part_unrelabel(self.h, ctypes.c_void_p(dist_pi_dev),
+                                       ctypes.c_void_p(dist_dev),
+                                       ctypes.c_void_p(stream) if stream else None))
+
+
+def bfs_partitioned_loopback(graph: CsrGraph, source: int, config: KernelConfig, world: int,
+                             device: int = 0, relabel: bool = True, parts=None):
+    """G-way partitioned traversal with all partitions on one device sharing
+    the full frontier bitmaps (the per-level allgather becomes a no-op).
+    Returns (distances in original ids, per-level records, partitions)."""
+    if parts is None:
+        dg = graph.device(device, 8)
+        p0 = PartitionedGraph(dg, 0, world, relabel)
+        parts = [p0] + [PartitionedGraph(dg, r, world, relabel, shared=p0)
+                        for r in range(1, world)]
+    for p in parts:
+        p.begin(source, config)
+    records = []
+    while True:
+        for p in parts:
+            p.step()
+        for p in parts:
+            p.sync()
+        results = [p.end_level() for p in parts]
+        done = results[0][0]
+        assert all(r[0] == done for r in results), "ranks disagree on termination"
+        rec = results[0][1]
+        rec.edges_examined = sum(r[1].edges_examined for r in results)
+        records.append(rec)
+        if done:
+            break
+    dist_pi = np.concatenate([p.local_distances() for p in parts])
+    return parts[0].unrelabel_host(dist_pi), records, parts
