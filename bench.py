@@ -260,6 +260,31 @@ def workload_config(args, graph):
             "parallelism": f"sources sharded over {args.gpus} GPU(s), graph replicated"}
 
 
+class _DeviceArray:
+    """Zero-copy torch view of library-owned device memory."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _peak_and_traffic(workload):
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    return float(peaks.get("hbm_gbs", 6650.0)), traffic
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -267,6 +292,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="rmat26", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--partitions", type=int, default=0,
+                    help="on one GPU: run the partitioned engine with this many loopback "
+                         "partitions (tests the multi-GPU path; N>1 under torchrun always "
+                         "partitions)")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=15.0)
@@ -276,19 +305,19 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.partitions > 1:
+        run_partitioned(args)
+    else:
+        run_single(args)
 
+
+def run_single(args):
     import torch
     import paper_2503_00430_b200 as pb
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist_on = world > 1
-    if dist_on:
-        import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     graph = build_graph(args.workload)
     cfg, stats = kernel_config(graph)
     offb = WORKLOADS[args.workload][3]
@@ -298,8 +327,7 @@ def main():
     log(f"[bench] resident on cuda:{local} in {upload_s:.1f}s, grid={dg.info['grid_blocks']}x"
         f"{dg.info['block_threads']}, {dg.info['device_bytes']/2**30:.2f} GiB")
 
-    all_sources = choose_sources(graph, dg, cfg, args.workload)
-    sources = [int(s) for s in all_sources[rank::world]]
+    sources = [int(s) for s in choose_sources(graph, dg, cfg, args.workload)]
     # A dedicated (non-default) stream: the kernel, the L2 flush and the
     # timing events must all be ordered on the same stream.
     stream = torch.cuda.Stream()
@@ -321,7 +349,7 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     ev = {s: [] for s in sources}
 
-    def step(timed: bool):
+    def step():
         pairs = []
         for s in sources:
             flush.zero_()
@@ -334,19 +362,18 @@ def main():
         return pairs
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     dg.sync(sptr)
     torch.cuda.synchronize()
-    if dist_on:
-        tdist.barrier()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     launches = 0
     with ClockSampler(local) as clocks:
+        time.sleep(1.0)  # let the sampler reach steady state before the timed region
         start.record(stream)
         recorded = []
         for _ in range(args.steps):
-            recorded.extend(step(True))
+            recorded.extend(step())
             launches += len(sources)
         end.record(stream)
         dg.sync(sptr)
@@ -357,52 +384,28 @@ def main():
         ev[s].append(a.elapsed_time(b))
     t_src = {s: statistics.mean(ev[s]) for s in sources}  # ms
 
-    # max over ranks of the step time; gather per-source figures
     ms_per_step = total_ms / args.steps
-    local_rows = [(s, e_r[s], b_alg[s], t_src[s]) for s in sources]
-    if dist_on:
-        gathered = [None] * world
-        tdist.all_gather_object(gathered, (ms_per_step, local_rows))
-        ms_per_step = max(x[0] for x in gathered)
-        rows = [r for x in gathered for r in x[1]]
-    else:
-        rows = local_rows
+    rows = [(s, e_r[s], b_alg[s], t_src[s]) for s in sources]
     gteps = [er / (t * 1e-3) / 1e9 for _, er, _, t in rows]
     value = harmonic(gteps)
     achieved = sum(b for _, _, b, _ in rows) / sum(t * 1e-3 for _, _, _, t in rows) / 1e9
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+    peak, traffic = _peak_and_traffic(args.workload)
 
     # e2e: the public API call with host buffers (pinned), D2H of the
-    # distance array inside the timed region, one pass over this rank's sources.
+    # distance array inside the timed region, one pass over the sources.
     host = pb.parbfs.pinned_empty(n, np.uint32)
     e2e_rows = []
     for s in sources:
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = dg.bfs(s, cfg, want_trace=False, out=host)
+        dg.bfs(s, cfg, want_trace=False, out=host)
         t1 = time.perf_counter()
         e2e_rows.append(e_r[s] / (t1 - t0) / 1e9)
-    if dist_on:
-        gathered = [None] * world
-        tdist.all_gather_object(gathered, e2e_rows)
-        e2e_rows = [x for g_ in gathered for x in g_]
     e2e_value = harmonic(e2e_rows)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         check = {}
         for s in sources[:2]:
             check[s] = dg.bfs(s, cfg, want_trace=False).distances.copy()
@@ -412,28 +415,242 @@ def main():
                "sample": sample, "parity_checked_sources": len(check),
                "parity_mismatches": mism}
 
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {**workload_config(args, graph),
+                                        "parallelism": "single GPU",
+                                        "graph_upload_s": round(upload_s, 2),
+                                        "mean_bfs_ms": round(statistics.mean(
+                                            t for *_, t in rows), 4)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "bfs_persistent (one cooperative launch per BFS)",
+                     "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
+                "h2d_bytes_per_step": 4 * NUM_SOURCES,
+                "d2h_bytes_per_step": 4 * n * NUM_SOURCES,
+                "note": "pbfs_bfs C-ABI call per source, distances copied to a pinned host "
+                        "buffer"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_partitioned(args):
+    """1D vertex partition: one partition per rank/GPU, one
+    in-place NCCL allgather of the next-frontier bitmap slices per level.
+    With one process and --partitions G, G loopback partitions share one GPU
+    (the allgather is then a no-op) -- the same code path, testable on 1 GPU."""
+    import torch
+    import paper_2503_00430_b200 as pb
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    multi = world > 1
+    if multi:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G = world if multi else args.partitions
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+
+    graph = None
+    if rank == 0:
+        graph = build_graph(args.workload)
+        cfg, _ = kernel_config(graph)
+        dg = graph.device(local, 8)
+        sources = [int(s) for s in choose_sources(graph, dg, cfg, args.workload)]
+        meta = [graph.vertex_count, graph.edge_count, int(cfg.force_top_down_only), sources]
+    else:
+        meta = [None]
+    t0 = time.time()
+    if multi:
+        box = [meta]
+        tdist.broadcast_object_list(box, src=0)
+        meta = box[0]
+    n, m, force_td, sources = meta
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid, force_top_down_only=bool(force_td))
+    if multi:
+        # Rank 0's device CSR -> every GPU over NCCL, then each rank builds its
+        # partition on device and drops the full copy.
+        if rank == 0:
+            arr = dg.device_arrays()
+            rowptr = torch.as_tensor(_DeviceArray(arr["row_offsets"], n + 1, "<i8"), device="cuda")
+            col = torch.as_tensor(_DeviceArray(arr["column_indices"], m, "<i4"), device="cuda")
+        else:
+            rowptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            col = torch.empty(m, dtype=torch.int32, device="cuda")
+        tdist.broadcast(rowptr, src=0)
+        tdist.broadcast(col, src=0)
+        torch.cuda.synchronize()
+        view = dict(vertex_count=n, edge_count=m, row_offsets=rowptr.data_ptr(),
+                    column_indices=col.data_ptr(), offset_bytes=8, symmetric=1)
+        parts = [pb.PartitionedGraph(view, rank, world, device=local)]
+        del rowptr, col
+        if rank == 0:
+            graph.release_device()
+        torch.cuda.empty_cache()
+    else:
+        parts = [pb.PartitionedGraph(dg, 0, G)]
+        parts += [pb.PartitionedGraph(dg, r, G, shared=parts[0]) for r in range(1, G)]
+    build_s = time.time() - t0
+    info0 = parts[0].info()
+    wl, wt = info0["words_local"], info0["words_total"]
+    log(f"[bench] {G} partitions built in {build_s:.1f}s, local arcs "
+        f"{[p.info()['local_arcs'] for p in parts]}")
+
+    launches = [0]
+
+    def exchange():
+        if multi:
+            nxt = parts[0].info()["next"]
+            full = torch.as_tensor(_DeviceArray(nxt, wt, "<i4"), device="cuda")
+            tdist.all_gather_into_tensor(full, full[rank * wl:(rank + 1) * wl])
+
+    def bfs(s):
+        for p in parts:
+            p.begin(s, cfg, sptr)
+        while True:
+            for p in parts:
+                p.step(sptr)
+                launches[0] += 3
+            exchange()
+            res = [p.end_level(sptr) for p in parts]
+            launches[0] += 2 * len(parts)
+            if res[0][0]:
+                return
+
+    def reduce_sum(vals):
+        if multi:
+            t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t)
+            return t.tolist()
+        return vals
+
+    def reduce_max(x):
+        if multi:
+            t = torch.tensor([x], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            return t.item()
+        return x
+
+    e_r, b_alg = {}, {}
+    for s in sources:
+        bfs(s)
+        nr = sum(p.component()[0] for p in parts)
+        ar = sum(p.component()[1] for p in parts)
+        nr, ar = reduce_sum([nr, ar])
+        e_r[s] = ar / 2.0
+        b_alg[s] = 4.0 * ar + 2.0 * 8 * nr + 4.0 * n
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    times = {s: [] for s in sources}
+    for _ in range(args.warmup):
+        for s in sources:
+            bfs(s)
+    torch.cuda.synchronize()
+    if multi:
+        tdist.barrier()
+    launches[0] = 0
+    with ClockSampler(local) as clocks:
+        time.sleep(1.0)
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            for s in sources:
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                bfs(s)
+                b.record(stream)
+                b.synchronize()
+                times[s].append(a.elapsed_time(b))
+        torch.cuda.synchronize()
+        wall_ms = (time.perf_counter() - t_all) * 1e3
+    clk = clocks.summary()
+
+    # e2e: traversal + distances gathered into original ids on rank 0's host
+    # (allgather of the pi-space slices, device un-relabel, pinned D2H).
+    nloc, npad = info0["local_count"], info0["padded_count"]
+    full_pi = torch.empty(npad, dtype=torch.int32, device="cuda")
+    dist_out = torch.empty(n, dtype=torch.int32, device="cuda")
+    host = pb.parbfs.pinned_empty(n, np.uint32)
+    host_t = torch.from_numpy(host.view(np.int32))
+    e2e_rows = []
+    for s in sources:
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bfs(s)
+        if multi:
+            dl = torch.as_tensor(_DeviceArray(parts[0].info()["dist_local"], nloc, "<i4"),
+                                 device="cuda")
+            tdist.all_gather_into_tensor(full_pi, dl)
+        else:
+            for r, p in enumerate(parts):
+                dl = torch.as_tensor(_DeviceArray(p.info()["dist_local"], nloc, "<i4"),
+                                     device="cuda")
+                full_pi[r * nloc:(r + 1) * nloc].copy_(dl)
+        parts[0].unrelabel(full_pi.data_ptr(), dist_out.data_ptr(), sptr)
+        if rank == 0:
+            host_t.copy_(dist_out, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_rows.append(e_r[s] / (reduce_max(time.perf_counter() - t0)) / 1e9)
+    e2e_value = harmonic(e2e_rows)
+    if rank == 0 and graph is not None:
+        # free parity check of the last traversal against the oracle
+        import oracle
+        want = oracle.port().bfs_serial(graph.row_offsets, graph.column_indices, sources[-1])
+        e2e_parity = bool(np.array_equal(host, want))
+    else:
+        e2e_parity = None
+
+    # per-source device time, max over ranks
+    t_src = {s: reduce_max(statistics.mean(times[s])) for s in sources}
+    ms_per_step = reduce_max(wall_ms / args.steps)
+    gteps = [e_r[s] / (t_src[s] * 1e-3) / 1e9 for s in sources]
+    value = harmonic(gteps)
+    achieved = sum(b_alg.values()) / sum(t * 1e-3 for t in t_src.values()) / 1e9
+    peak, _ = _peak_and_traffic(args.workload)
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": {**workload_config(args, graph),
-                                            "graph_upload_s": round(upload_s, 2),
-                                            "mean_bfs_ms": round(statistics.mean(
-                                                t for *_, t in rows), 4)},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "bfs_persistent (one cooperative launch per BFS)",
-                         "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source"},
-            "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4 * NUM_SOURCES,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "description": WORKLOADS[args.workload][4],
+                       "vertices": n, "directed_arcs": m, "offset_bytes": 8,
+                       "sources": NUM_SOURCES, "source_seed": SOURCE_SEED,
+                       "graph_seed": GRAPH_SEED, "variant": "hybrid",
+                       "parallelism": (f"1D vertex partition over {world} GPUs, hashed relabel, "
+                                       "per-level NCCL allgather of the frontier bitmap")
+                       if multi else f"{G} loopback partitions on one GPU (path test)",
+                       "l2": "flushed (512 MiB memset) between traversals",
+                       "partition_build_s": round(build_s, 2),
+                       "mean_bfs_ms": round(statistics.mean(t_src.values()), 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peak * max(world, 1), "unit": "GB/s",
+                         "frac": round(achieved / (peak * max(world, 1)), 4), "traffic": None,
+                         "kernel": "partitioned level kernels (all ranks)",
+                         "bytes_model": "B_alg = 4*A_r + 2*8*N_r + 4*N per source"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": 4 * NUM_SOURCES,
                     "d2h_bytes_per_step": 4 * n * NUM_SOURCES,
-                    "note": "pbfs_bfs C-ABI call per source, distances copied to a host buffer"},
-            "gpu_launches": launches * world,
+                    "note": "partitioned traversal + allgather of distance slices + device "
+                            "un-relabel + pinned D2H on rank 0",
+                    "parity_vs_oracle_last_source": e2e_parity},
+            "gpu_launches": launches[0] * max(world, 1),
             "clocks": clk,
         }
         print(json.dumps(out), flush=True)
-    if dist_on:
+    if multi:
         tdist.destroy_process_group()
 
 

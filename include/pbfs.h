@@ -287,7 +287,15 @@ pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offse
                                      const uint32_t** column_indices, uint32_t* offset_bytes);
 pbfs_status pbfs_part_create(const pbfs_graph* full, const pbfs_part_options* opt,
                              pbfs_part** out);
+/* Same, from a device CSR view (row_offsets / column_indices are DEVICE
+ * pointers on `device`, e.g. buffers received by a broadcast); only read
+ * during the call. */
+pbfs_status pbfs_part_create_device(const pbfs_csr* device_csr, int32_t device,
+                                    const pbfs_part_options* opt, pbfs_part** out);
 pbfs_status pbfs_part_destroy(pbfs_part* p);
+/* This rank's share of the reached-component figures of the last traversal
+ * (owned vertices only; sum over ranks = N_r, A_r). */
+pbfs_status pbfs_part_component(pbfs_part* p, uint64_t* n_reached, uint64_t* arcs_reached);
 pbfs_status pbfs_part_get_info(const pbfs_part* p, pbfs_part_info* info);
 pbfs_status pbfs_part_relabel(const pbfs_part* p, uint64_t v, uint64_t* pi_v);
 pbfs_status pbfs_part_begin(pbfs_part* p, uint32_t source, const pbfs_config* cfg, void* stream);

@@ -111,7 +111,9 @@ SIGNATURES = [
     ("pbfs_load_csr1", ctypes.c_int, [ctypes.c_char_p, P(c_vp)]),
     ("pbfs_graph_device_arrays", ctypes.c_int, [c_vp, P(c_vp), P(c_vp), P(c_u32)]),
     ("pbfs_part_create", ctypes.c_int, [c_vp, P(PartOptions), P(c_vp)]),
+    ("pbfs_part_create_device", ctypes.c_int, [P(Csr), c_i32, P(PartOptions), P(c_vp)]),
     ("pbfs_part_destroy", ctypes.c_int, [c_vp]),
+    ("pbfs_part_component", ctypes.c_int, [c_vp, P(c_u64), P(c_u64)]),
     ("pbfs_part_get_info", ctypes.c_int, [c_vp, P(PartInfo)]),
     ("pbfs_part_relabel", ctypes.c_int, [c_vp, c_u64, P(c_u64)]),
     ("pbfs_part_begin", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),

@@ -425,22 +425,56 @@ pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* co
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void* rowptr,
+                             const uint32_t* col, uint32_t offb, const pbfs_part_options* opt,
+                             pbfs_part** out);
+}  // namespace
+
+extern "C" {
+
 pbfs_status pbfs_part_create(const pbfs_graph* full, const pbfs_part_options* opt,
                              pbfs_part** out) {
   if (!full || !opt || !out) return fail(PBFS_E_INPUT, "null argument");
-  if (opt->world < 1 || opt->rank >= opt->world) return fail(PBFS_E_CONFIG, "bad rank/world");
   pbfs_graph_info gi;
   pbfs_status st = pbfs_graph_get_info(full, &gi);
   if (st != PBFS_OK) return st;
-  if (!gi.symmetric) {
-    return fail(PBFS_E_INPUT, "the vertex partition needs a symmetric graph (its column "
-                              "slice is the transpose of the row slice)");
-  }
   const void* rowptr = nullptr;
   const uint32_t* col = nullptr;
   uint32_t offb = 0;
   if ((st = pbfs_graph_device_arrays(full, &rowptr, &col, &offb)) != PBFS_OK) return st;
+  return part_create_impl(gi.vertex_count, gi.symmetric != 0, gi.device, rowptr, col, offb, opt,
+                          out);
+}
 
+pbfs_status pbfs_part_create_device(const pbfs_csr* dcsr, int32_t device,
+                                    const pbfs_part_options* opt, pbfs_part** out) {
+  if (!dcsr || !opt || !out) return fail(PBFS_E_INPUT, "null argument");
+  if (dcsr->offset_bytes != 4 && dcsr->offset_bytes != 8) {
+    return fail(PBFS_E_FORMAT, "offset width must be 4 or 8 bytes");
+  }
+  return part_create_impl(dcsr->vertex_count, dcsr->symmetric != 0, device, dcsr->row_offsets,
+                          dcsr->column_indices, dcsr->offset_bytes, opt, out);
+}
+
+}  // extern "C"
+
+namespace {
+pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void* rowptr,
+                             const uint32_t* col, uint32_t offb, const pbfs_part_options* opt,
+                             pbfs_part** out) {
+  if (opt->world < 1 || opt->rank >= opt->world) return fail(PBFS_E_CONFIG, "bad rank/world");
+  if (!symmetric) {
+    return fail(PBFS_E_INPUT, "the vertex partition needs a symmetric graph (its column "
+                              "slice is the transpose of the row slice)");
+  }
+  pbfs_status st;
+  struct {
+    uint64_t vertex_count;
+    int32_t device;
+  } gi{n, device};
   auto* g = new (std::nothrow) pbfs_part;
   if (!g) return fail(PBFS_E_CAPACITY, "host allocation failed");
   g->device = gi.device;
@@ -503,6 +537,9 @@ pbfs_status pbfs_part_create(const pbfs_graph* full, const pbfs_part_options* op
   *out = g;
   return PBFS_OK;
 }
+}  // namespace
+
+extern "C" {
 
 pbfs_status pbfs_part_destroy(pbfs_part* g) {
   part_release(g);
@@ -653,6 +690,22 @@ pbfs_status pbfs_part_unrelabel(pbfs_part* g, const uint32_t* dist_pi, uint32_t*
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
   k_unrelabel<<<g->grid, 256, 0, s>>>(dist_pi, g->n, g->rl, dist);
   PCUDA(cudaGetLastError(), "unrelabel");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_component(pbfs_part* g, uint64_t* n_reached, uint64_t* arcs_reached) {
+  if (!g || !n_reached || !arcs_reached) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(&g->ctl->cnt[2]);
+  PCUDA(cudaMemsetAsync(out, 0, 16, g->stream), "memset");
+  // component_kernel (pbfs_kernels.cuh) over the row slice: local degrees.
+  component_kernel<unsigned long long><<<g->grid, 256, 0, g->stream>>>(g->rowloc, g->dist,
+                                                                         g->nloc, out);
+  unsigned long long h[2];
+  PCUDA(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, g->stream), "read");
+  PCUDA(cudaStreamSynchronize(g->stream), "component");
+  *n_reached = h[0];
+  *arcs_reached = h[1];
   return PBFS_OK;
 }
 

@@ -518,6 +518,17 @@ class DeviceGraph:
     def sync(self, stream: int = 0) -> None:
         _check(lib.pbfs_graph_sync(self.h, ctypes.c_void_p(stream) if stream else None))
 
+    def device_arrays(self) -> dict:
+        """Device CSR view (pointers into this handle's HBM copy)."""
+        r = ctypes.c_void_p()
+        c = ctypes.c_void_p()
+        ob = ctypes.c_uint32()
+        _check(lib.pbfs_graph_device_arrays(self.h, ctypes.byref(r), ctypes.byref(c),
+                                            ctypes.byref(ob)))
+        return dict(vertex_count=self.info["vertex_count"], edge_count=self.info["edge_count"],
+                    row_offsets=r.value, column_indices=c.value, offset_bytes=ob.value,
+                    symmetric=self.info["symmetric"])
+
     def device_distances_ptr(self) -> int:
         p = ctypes.c_void_p()
         _check(lib.pbfs_graph_device_dist(self.h, ctypes.byref(p)))
@@ -658,17 +669,37 @@ class PartitionedGraph:
     words per rank, e.g. NCCL over NVLink), then ``end_level()``.
     """
 
-    def __init__(self, dgraph: DeviceGraph, rank: int, world: int, relabel: bool = True,
-                 shared: Optional["PartitionedGraph"] = None):
+    def __init__(self, dgraph, rank: int, world: int, relabel: bool = True,
+                 shared: Optional["PartitionedGraph"] = None, device: int = 0):
+        """dgraph: a DeviceGraph, or a device CSR view dict(vertex_count,
+        edge_count, row_offsets=<device ptr>, column_indices=<device ptr>,
+        offset_bytes, symmetric) on `device`."""
         opt = L.PartOptions()
         opt.rank, opt.world, opt.relabel = int(rank), int(world), int(bool(relabel))
         if shared is not None:
             si = shared.info()
             opt.shared_frontier, opt.shared_next = si["frontier"], si["next"]
         h = ctypes.c_void_p()
-        _check(lib.pbfs_part_create(dgraph.h, ctypes.byref(opt), ctypes.byref(h)))
+        if isinstance(dgraph, DeviceGraph):
+            _check(lib.pbfs_part_create(dgraph.h, ctypes.byref(opt), ctypes.byref(h)))
+        else:
+            c = L.Csr()
+            c.vertex_count = int(dgraph["vertex_count"])
+            c.edge_count = int(dgraph["edge_count"])
+            c.row_offsets = int(dgraph["row_offsets"])
+            c.column_indices = int(dgraph["column_indices"])
+            c.offset_bytes = int(dgraph["offset_bytes"])
+            c.symmetric = int(bool(dgraph["symmetric"]))
+            _check(lib.pbfs_part_create_device(ctypes.byref(c), int(device), ctypes.byref(opt),
+                                               ctypes.byref(h)))
         self.h = h
         self._keep = (dgraph, shared)
+
+    def component(self):
+        nr = ctypes.c_uint64()
+        ar = ctypes.c_uint64()
+        _check(lib.pbfs_part_component(self.h, ctypes.byref(nr), ctypes.byref(ar)))
+        return nr.value, ar.value
 
     def close(self):
         if getattr(self, "h", None):
