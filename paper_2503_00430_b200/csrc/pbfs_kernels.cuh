@@ -52,6 +52,7 @@ constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
+constexpr int kBarGroups = 16;  // grid-barrier arrival groups
 
 enum Claim : int { kClaimCas = 0, kClaimPlain = 1, kClaimBitmap = 2 };
 enum Policy : int { kPolicyTopDown = 0, kPolicyFraction = 1, kPolicyBeamer = 2 };
@@ -73,8 +74,9 @@ struct alignas(128) LevelCnt {
 };
 
 struct alignas(128) Ctl {
-  unsigned long long bar_count;  // monotone arrivals (grid barrier)
+  unsigned long long bar_count;  // monotone group completions (grid barrier)
   unsigned long long pad0[15];
+  unsigned long long bar_sub[kBarGroups][16];  // per-group arrivals, one line each
   unsigned int exit_count;
   unsigned int pad1[31];
   LevelCnt cnt[4];
@@ -179,19 +181,27 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   return v;
 }
 
-// Sense-free grid barrier on a monotone 64-bit arrival counter: barrier k
-// completes when the counter reaches k * gridDim.x. Thread 0 of each CTA
-// publishes the CTA's writes (fence), arrives, spins with acquire loads, and
-// fences again so the whole CTA observes every other CTA's writes.
+// Sense-free two-level grid barrier on monotone 64-bit counters. CTA b
+// arrives on group counter b % kBarGroups (own 128 B line); the group's last
+// arriver of barrier k bumps the top counter, which every CTA polls until it
+// reaches k * groups. ~gridDim/16 serialised atomics per L2 line instead of
+// gridDim on one. Thread 0 publishes the CTA's writes (fence) before
+// arriving and fences again after, so the whole CTA observes every other
+// CTA's writes.
 struct GridBarrier {
   Ctl* ctl;
-  unsigned long long target;
+  unsigned long long k;  // barriers completed in this launch
   __device__ __forceinline__ void sync() {
     __syncthreads();
-    target += gridDim.x;
+    ++k;
     if (threadIdx.x == 0) {
+      const unsigned groups = gridDim.x < kBarGroups ? gridDim.x : kBarGroups;
+      const unsigned g = blockIdx.x % groups;
+      const unsigned long long size = (gridDim.x - g + groups - 1) / groups;
       __threadfence();
-      atomicAdd(&ctl->bar_count, 1ull);
+      const unsigned long long old = atomicAdd(&ctl->bar_sub[g][0], 1ull);
+      if (old == k * size - 1) atomicAdd(&ctl->bar_count, 1ull);
+      const unsigned long long target = k * groups;
       // Relaxed polling: an acquire load per spin would invalidate this SM's
       // L1 on every iteration (CCTL.IVALL) under the other resident CTAs.
       while (ld_relaxed64(&ctl->bar_count) < target) __nanosleep(32);
@@ -453,6 +463,9 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
     }
     if (hub) deg = 0;
     td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t, obm);
+    // The static first slices cover small frontiers entirely: no cursor
+    // round trip at all (the common case on deep, narrow graphs).
+    if (qlen <= (unsigned long long)warps_total * 32) break;
     unsigned int nb = 0;
     if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
     base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
@@ -849,6 +862,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     const unsigned int out = atomicAdd(&ctl->exit_count, 1u);
     if (out == gridDim.x - 1) {
       ctl->bar_count = 0;
+      for (int i = 0; i < kBarGroups; ++i) ctl->bar_sub[i][0] = 0;
       ctl->exit_count = 0;
       __threadfence();
     }
