@@ -256,8 +256,10 @@ def workload_config(args, graph):
     return {"workload": args.workload, "description": desc, "vertices": graph.vertex_count,
             "directed_arcs": graph.edge_count, "offset_bytes": offb, "sources": NUM_SOURCES,
             "source_seed": SOURCE_SEED, "graph_seed": GRAPH_SEED, "variant": "hybrid",
-            "l2": "flushed (512 MiB memset) between launches",
-            "parallelism": f"sources sharded over {args.gpus} GPU(s), graph replicated"}
+            "l2": ("flushed (512 MiB memset) between launches" if args.impl == "ours"
+                   else "n/a (host CPU)"),
+            "parallelism": (f"{args.gpus} GPU(s)" if args.impl == "ours"
+                            else f"reference std::thread workers on {os.cpu_count()} host cores")}
 
 
 class _DeviceArray:

@@ -175,6 +175,20 @@ __device__ __forceinline__ void red_or_if(bool pred, uint32_t* addr, uint32_t va
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
       "@q red.global.or.b32 [%1], %2;\n\t}" ::"r"((uint32_t)pred), "l"(addr), "r"(val));
 }
+// Read-only graph arrays (`col`, `rowptr`) streamed without allocating in L1:
+// L1 is kept for the skewed visited / frontier bitmap probes, where RMAT hub
+// words hit (measured: L1-cacheable skewed probes 380 G/s vs 125 G/s at L2,
+// tools/ubench_probe.cu).
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_stream(const unsigned long long* p) {
+  unsigned long long v;
+  asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -270,22 +284,20 @@ struct WarpPush {
 
 template <typename OffT>
 __device__ __forceinline__ unsigned long long degree_of(const Params<OffT>& p, uint32_t v) {
-  return (unsigned long long)(__ldg(&p.rowptr[v + 1]) - __ldg(&p.rowptr[v]));
+  return (unsigned long long)(ld_stream(&p.rowptr[v + 1]) - ld_stream(&p.rowptr[v]));
 }
 
 struct WarpTally {
   unsigned long long produced = 0, raw = 0, edges = 0, degree = 0, viol = 0;
 };
 
-// Probe word for the claim test, read at L2 (ld.global.cg): an L1 copy would
-// never see other SMs' claims made during the level, so every edge into a
-// not-yet-claimed vertex would go on to issue an L2 atomic. At L2 the probe
-// sees a claim as soon as it lands, which keeps atomics close to one per
-// discovered vertex.
+// Probe word for the claim test. kClaimBitmap probes `visited` through L1
+// first (see claim_batch); the dist probes of the CAS / plain variants go to
+// L2 (random 4 B over n words, no reuse).
 template <int C, typename OffT>
 __device__ __forceinline__ uint32_t probe_word(const Params<OffT>& p, uint32_t v) {
   if constexpr (C == kClaimBitmap) {
-    return __ldcg(&p.visited[v >> 5]);
+    return __ldca(&p.visited[v >> 5]);
   } else {
     return __ldcg(&p.dist[v]);
   }
@@ -326,6 +338,18 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
     (void)wp;
     (void)cnt;
   } else {
+    if constexpr (C == kClaimBitmap) {
+      // Stage 1b: an L1 hit is authoritative for bits set before this level
+      // (the grid barrier's fence invalidated L1) -- RMAT hub words stay hot
+      // there and never touch the hot L2 slices. A clear bit may be stale
+      // with respect to this level's claims, so it is re-probed at L2 before
+      // paying for an atomic.
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t bit = 1u << (v[k] & 31);
+        w[k] = ld_cg_if(((okm >> k) & 1u) && !(w[k] & bit), &p.visited[v[k] >> 5], w[k]);
+      }
+    }
     // Stage 2: predicated claim atomics, all issued before any result is used.
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -403,7 +427,7 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
       okm |= (uint32_t)ok << k;
       // Dead slots re-read the batch's first edge (always valid): no branch.
       const unsigned long long ei = ok ? (unsigned long long)ob + (e - oex) : (unsigned long long)b0;
-      v[k] = __ldcs(&p.col[ei]);
+      v[k] = ld_stream(&p.col[ei]);
     }
     claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
   }
@@ -500,7 +524,7 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
         const uint32_t e = e0 + 32 * k + lane;
         const bool ok = e < len;
         okm |= (uint32_t)ok << k;
-        v[k] = __ldcs(&base[ok ? e : 0u]);
+        v[k] = ld_stream(&base[ok ? e : 0u]);
       }
       claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
     }
@@ -576,7 +600,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
 #pragma unroll
         for (int c = 0; c < C0; ++c) {
           const OffT e = beg[q] + c < end[q] ? beg[q] + c : beg[q];
-          u[q][c] = __ldcs(&p.col[e]);
+          u[q][c] = __ldg(&p.col[e]);
         }
       }
 #pragma unroll
@@ -606,7 +630,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
           for (OffT e0 = beg[q] + C0; !hit && e0 < end[q]; e0 += 8) {
             uint32_t x[8], fx[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = __ldcs(&p.col[e0 + c < end[q] ? e0 + c : e0]);
+            for (int c = 0; c < 8; ++c) x[c] = __ldg(&p.col[e0 + c < end[q] ? e0 + c : e0]);
 #pragma unroll
             for (int c = 0; c < 8; ++c) fx[c] = front[x[c] >> 5];
             unsigned hm = 0;
