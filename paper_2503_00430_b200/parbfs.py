@@ -151,6 +151,9 @@ class KernelConfig:
     force_top_down_only: bool = False
     validate_same_value_stores: bool = False
     racy_visited_claim: bool = False
+    # kernel_config.hpp:26-36: called once per frontier (the seed, then every
+    # produced level) with a LevelSnapshot. Test instrumentation only.
+    level_observer: Optional[Callable] = None
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -378,6 +381,44 @@ def pick_sources(graph: CsrGraph, count: int, seed: int = 1) -> np.ndarray:
     return out
 
 
+def load_edge_list(path: str, one_based: bool = False, symmetrize: bool = True,
+                   vertex_count_hint: Optional[int] = None) -> CsrGraph:
+    """edge_list.cpp:26-82: whitespace "u v" lines, '#'/'%' comments and blank
+    lines skipped, trailing fields ignored, one-based ids shifted, vertex
+    count = max id + 1 unless a (larger) hint is given."""
+    pairs = []
+    max_seen = -1
+    try:
+        fh = open(path)
+    except OSError:
+        raise InputError(f"cannot open edge list file: {path}")
+    with fh:
+        for line_no, line in enumerate(fh, 1):
+            stripped = line.strip(" \t\r\n")
+            if not stripped or stripped[0] in "#%":
+                continue
+            fields = stripped.split()
+            try:
+                a, b = int(fields[0]), int(fields[1])
+            except (ValueError, IndexError):
+                raise InputError(f"{path}:{line_no}: expected two integer vertex ids")
+            if one_based:
+                a, b = a - 1, b - 1
+            if a < 0 or b < 0:
+                raise InputError(f"{path}:{line_no}: vertex id below the index base")
+            if a > MAX_VERTEX_COUNT or b > MAX_VERTEX_COUNT:
+                raise InputError(f"{path}:{line_no}: vertex id exceeds the supported maximum")
+            pairs.append((a, b))
+            max_seen = max(max_seen, a, b)
+    n = max_seen + 1
+    if vertex_count_hint is not None:
+        if vertex_count_hint < n:
+            raise InputError(f"{path}: declared vertex count {vertex_count_hint} is smaller "
+                             f"than the largest referenced vertex + 1 ({n})")
+        n = vertex_count_hint
+    return build_csr(np.array(pairs, dtype=np.int64).reshape(-1, 2), n, symmetrize)
+
+
 def save_binary_csr(graph: CsrGraph, path: str) -> None:
     """graph_io.cpp:70-85."""
     v = graph._view()
@@ -552,6 +593,32 @@ def pinned_empty(count: int, dtype=np.uint32) -> np.ndarray:
     return np.frombuffer(buf, dtype=dtype, count=int(count))
 
 
+@dataclass
+class LevelSnapshot:
+    """kernel_config.hpp:26-33."""
+    depth: int
+    produced_by: TraversalPhase
+    entries: np.ndarray
+
+
+def _emit_snapshots(result: BfsResult, observer: Callable) -> None:
+    """LevelObserver parity (kernels.cpp:158-161,466-481): one snapshot for the
+    seed frontier, then one per produced level, in depth order. The device
+    frontiers carry no duplicates (claims are exact), so each snapshot is the
+    ascending set of vertices first reached at that depth -- what the
+    reference's observers see after their sort + unique."""
+    d = result.distances
+    reached = d != UNREACHED
+    order = np.argsort(d[reached], kind="stable")
+    ids = np.nonzero(reached)[0][order].astype(np.uint32)
+    levels = d[reached][order]
+    bounds = np.searchsorted(levels, np.arange(int(levels.max()) + 2 if levels.size else 1))
+    recs = result.trace.records
+    for depth in range(len(bounds) - 1):
+        phase = TraversalPhase.TopDown if depth == 0 else recs[depth - 1].phase
+        observer(LevelSnapshot(depth, phase, ids[bounds[depth]:bounds[depth + 1]]))
+
+
 def _gpu_run(graph: CsrGraph, source: int, config: KernelConfig, variant: KernelVariant,
              device: int = 0) -> BfsResult:
     cfg = KernelConfig(**{**config.__dict__, "variant": variant})
@@ -559,7 +626,10 @@ def _gpu_run(graph: CsrGraph, source: int, config: KernelConfig, variant: Kernel
     if not (0 <= int(source) < graph.vertex_count):
         raise InputError(f"source vertex {source} is out of range for a graph with "
                          f"{graph.vertex_count} vertices")
-    return graph.device(device).bfs(source, cfg)
+    res = graph.device(device).bfs(source, cfg)
+    if config.level_observer is not None:
+        _emit_snapshots(res, config.level_observer)
+    return res
 
 
 def bfs_conventional(graph: CsrGraph, source: int, config: KernelConfig) -> BfsResult:
@@ -605,7 +675,10 @@ def run_bfs(graph: CsrGraph, source: int, config: KernelConfig, stats: GraphStat
     if not (0 <= int(source) < graph.vertex_count):
         raise InputError(f"source vertex {source} is out of range for a graph with "
                          f"{graph.vertex_count} vertices")
-    return graph.device(device).bfs(source, effective)
+    res = graph.device(device).bfs(source, effective)
+    if config.level_observer is not None:
+        _emit_snapshots(res, config.level_observer)
+    return res
 
 
 # ---- timing (timing.hpp:17-34, timing.cpp:33-77) -------------------------------------
