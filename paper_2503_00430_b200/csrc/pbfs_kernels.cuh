@@ -45,9 +45,15 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_SLOTS
 #define PBFS_SLOTS 8  // edge slots per lane in the top-down batches
 #endif
+#ifndef PBFS_HEAVY_DEG
+#define PBFS_HEAVY_DEG 128
+#endif
+#ifndef PBFS_CHUNK
+#define PBFS_CHUNK 512
+#endif
 constexpr int kMinBlocks = PBFS_MIN_BLOCKS;  // resident CTAs per SM the register budget targets
-constexpr uint32_t kHeavyDeg = 1024; // degree above which a vertex is split
-constexpr uint32_t kChunk = 2048;    // edges per heavy work item
+constexpr uint32_t kHeavyDeg = PBFS_HEAVY_DEG;  // degree above which a vertex is split
+constexpr uint32_t kChunk = PBFS_CHUNK;  // edges per heavy work item
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
@@ -102,6 +108,7 @@ struct Params {
   uint32_t* visited;
   uint32_t* bm[2];
   const uint32_t* init_mask;
+  const uint32_t* __restrict__ first_nbr;  // col[rowptr[v]] (0 for isolated v), n entries
   uint32_t* queue[2];
   HeavyItem* heavy;
   Ctl* ctl;
@@ -580,69 +587,53 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
     if (owner) found[lane] = 0;
     __syncwarp();
     for (uint32_t k = 0; k < total; k += 32 * KB) {
-      constexpr int C0 = 4;  // first chunk of neighbours per vertex
-      uint32_t v[KB], u[KB][C0], fw[KB][C0];
-      OffT beg[KB], end[KB];
+      uint32_t v[KB], u0[KB], f0[KB];
       bool valid[KB];
-      // Branch-free loads (dead slots read vertex list[0]'s data, out-of-range
-      // neighbour slots re-read the first one; `col` is padded so col[m] is
-      // readable) so ptxas keeps every load of the batch in flight together.
+      // Stage 1: the first neighbour of each vertex from the dense first_nbr
+      // array (coalesced: the list is ascending) and its frontier word. On
+      // RMAT nearly every vertex that has a frontier parent finds it here, so
+      // rowptr / col are not read at all for it. Branch-free loads (dead
+      // slots read list[0]'s data) keep every load of the batch in flight.
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
         const uint32_t idx = k + 32 * q + lane;
         valid[q] = idx < total;
         v[q] = list[valid[q] ? idx : 0];
-        beg[q] = __ldg(&p.rowptr[v[q]]);
-        end[q] = __ldg(&p.rowptr[v[q] + 1]);
+        u0[q] = __ldg(&p.first_nbr[v[q]]);
       }
 #pragma unroll
-      for (int q = 0; q < KB; ++q) {
-#pragma unroll
-        for (int c = 0; c < C0; ++c) {
-          const OffT e = beg[q] + c < end[q] ? beg[q] + c : beg[q];
-          u[q][c] = __ldg(&p.col[e]);
-        }
-      }
+      for (int q = 0; q < KB; ++q) f0[q] = front[u0[q] >> 5];
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
-#pragma unroll
-        for (int c = 0; c < C0; ++c) fw[q][c] = front[u[q][c] >> 5];
-        if (!valid[q]) end[q] = beg[q];
-      }
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        if (beg[q] >= end[q]) continue;
+        if (!valid[q]) continue;
         // kernels.cpp:362-374: first frontier neighbour wins (early exit);
         // edges count up to and including it.
-        const unsigned long long deg = (unsigned long long)(end[q] - beg[q]);
-        unsigned hitmask = 0;
-#pragma unroll
-        for (int c = 0; c < C0; ++c) {
-          hitmask |= (unsigned)((c < (long long)deg) && ((fw[q][c] >> (u[q][c] & 31)) & 1u)) << c;
+        bool hit = (f0[q] >> (u0[q] & 31)) & 1u;
+        unsigned long long scanned = 1;
+        OffT beg = 0, end = 0;
+        if (!hit || p.policy == kPolicyBeamer) {
+          beg = __ldg(&p.rowptr[v[q]]);
+          end = __ldg(&p.rowptr[v[q] + 1]);
         }
-        unsigned long long scanned;
-        bool hit = hitmask != 0;
-        if (hit) {
-          scanned = (unsigned long long)__ffs(hitmask);
-        } else {
-          scanned = deg < (unsigned long long)C0 ? deg : (unsigned long long)C0;
-          // Continue in chunks of 8: all loads of a chunk in flight together.
-          for (OffT e0 = beg[q] + C0; !hit && e0 < end[q]; e0 += 8) {
+        if (!hit) {
+          // Continue from the second neighbour in chunks of 8: all loads of
+          // a chunk in flight together.
+          for (OffT e0 = beg + 1; !hit && e0 < end; e0 += 8) {
             uint32_t x[8], fx[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = __ldg(&p.col[e0 + c < end[q] ? e0 + c : e0]);
+            for (int c = 0; c < 8; ++c) x[c] = __ldg(&p.col[e0 + c < end ? e0 + c : e0]);
 #pragma unroll
             for (int c = 0; c < 8; ++c) fx[c] = front[x[c] >> 5];
             unsigned hm = 0;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              hm |= (unsigned)(e0 + c < end[q] && ((fx[c] >> (x[c] & 31)) & 1u)) << c;
+              hm |= (unsigned)(e0 + c < end && ((fx[c] >> (x[c] & 31)) & 1u)) << c;
             }
             if (hm) {
               hit = true;
               scanned += (unsigned long long)__ffs(hm);
             } else {
-              const OffT rem = end[q] - e0;
+              const OffT rem = end - e0;
               scanned += rem < 8 ? (unsigned long long)rem : 8ull;
             }
           }
@@ -652,7 +643,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
           p.dist[v[q]] = nd;
           atomicOr(&found[(v[q] >> 5) - g * kGroupWords], 1u << (v[q] & 31));
           ++t.produced;
-          if (p.policy == kPolicyBeamer) t.degree += deg;
+          if (p.policy == kPolicyBeamer) t.degree += (unsigned long long)(end - beg);
         }
       }
     }

@@ -148,6 +148,14 @@ __global__ void k_col_stats(const unsigned long long* __restrict__ colptr, uint6
   if (hv) atomicAdd(heavy_items, hv);
 }
 
+__global__ void k_first_nbr(const unsigned long long* __restrict__ rowloc,
+                            const uint32_t* __restrict__ colrow, uint64_t nloc, uint32_t* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    first[i] = rowloc[i] < rowloc[i + 1] ? colrow[rowloc[i]] : 0u;
+  }
+}
+
 __global__ void k_local_mask(const unsigned long long* __restrict__ rowloc, uint64_t nloc,
                              uint64_t words, uint32_t* mask) {
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
@@ -280,6 +288,7 @@ struct pbfs_part {
   // row slice (bottom-up)
   unsigned long long* rowloc = nullptr;  // nloc + 1
   uint32_t* colrow = nullptr;            // m_loc, global pi-ids
+  uint32_t* first = nullptr;             // nloc + 1: first row-slice neighbour
   // column slice (top-down)
   unsigned long long* colptr = nullptr;  // npad + 1
   uint32_t* colcol = nullptr;            // m_loc, local ids
@@ -361,6 +370,7 @@ Params<unsigned long long> bu_params(const pbfs_part* g) {
   Params<unsigned long long> p{};
   p.rowptr = g->rowloc;
   p.col = g->colrow;
+  p.first_nbr = g->first;
   p.dist = g->dist;
   p.visited = g->visited;
   p.ctl = g->ctl;
@@ -412,6 +422,8 @@ pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* co
   unsigned long long hs[2];
   PCUDA(cudaMemcpyAsync(hs, stats, 16, cudaMemcpyDeviceToHost, s), "read stats");
   if ((st = palloc(g, &g->mask, g->lwords * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  if ((st = palloc(g, &g->first, (g->nloc + 1) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  k_first_nbr<<<blocks, 256, 0, s>>>(g->rowloc, g->colrow, g->nloc, g->first);
   k_local_mask<<<blocks, 256, 0, s>>>(g->rowloc, g->nloc, g->lwords, g->mask);
   PCUDA(cudaGetLastError(), "partition kernels");
   PCUDA(cudaStreamSynchronize(s), "partition build");
