@@ -10,10 +10,16 @@ source's launch over the K timed steps; E_r = (sum of reached degrees) / 2.
 
   python bench.py [--workload rmat26] [--steps K] [--warmup W] [--gpus N]
   python bench.py --impl reference ...   # the reference's own CPU hybrid BFS
+  python bench.py --partitions G         # partitioned engine, G loopback partitions on 1 GPU
 
-Multi-GPU (torchrun, N > 1): the 64 sources are sharded across ranks, every
-rank holding the whole graph (independent traversals, no data-path
-collective): "scaling": "weak" in sources per GPU; timing is max over ranks.
+Multi-GPU (torchrun, N > 1): the graph is 1D vertex-partitioned over the
+ranks (hashed relabel; rank 0 generates it and broadcasts the device CSR over
+NCCL; each rank builds its row/column slices on device), one in-place NCCL
+allgather of the next-frontier bitmap per level; "scaling": "strong" (fixed
+graph), per-source time = max over ranks.
+
+PBFS_GRAPH_CACHE_DIR=DIR caches generated graphs (numpy arrays) for repeated
+runs inside one session.
 """
 from __future__ import annotations
 

@@ -6,27 +6,37 @@
 // between levels (the reference needs a std::barrier round and a serial
 // single-worker section per level, kernels.cpp:165-173,384-464). Per level:
 //
-//   top-down  (kernels.cpp:262-338): warps grab 32-entry slices of the frontier
-//     queue; vertices of degree <= kHeavyDeg are expanded warp-cooperatively
-//     (shuffle scan of degrees + per-lane owner search, so a warp reads one
-//     coalesced 128 B span of `col` per step); hubs are split into
-//     kChunk-edge items expanded by the whole grid after a barrier. Claims:
+//   top-down  (kernels.cpp:262-338): warps take 32-entry frontier slices
+//     (static first slice, atomic cursor only for large frontiers); vertices
+//     of degree <= kHeavyDeg are expanded warp-cooperatively (shuffle scan of
+//     degrees, kSlots edge slots per lane, owner found by a shuffle binary
+//     search); hubs are split into kChunk-edge items reserved with one
+//     atomicAdd per warp and expanded by the whole grid after a barrier, 32
+//     consecutive sorted neighbours per warp load. Every batch issues all its
+//     col loads, then all probes, then all claim atomics (predicated, no
+//     branches) before consuming any result. Claims:
 //       kClaimCas    atomicCAS on dist            (BFS-Conventional)
-//       kClaimPlain  plain same-value dist stores (BFS-NonAtomic, duplicates)
-//       kClaimBitmap test-then-atomicOr on the bit-packed visited set, then a
-//                    plain dist store            (BFS-Hybrid / VisitedBitmap)
-//     Discoveries go to a per-warp shared-memory buffer flushed with one
-//     atomicAdd per 256 entries (the GPU form of LocalFrontier +
+//       kClaimPlain  plain same-value dist stores + idempotent red.or into a
+//                    next-frontier bitmap         (BFS-NonAtomic, duplicates)
+//       kClaimBitmap visited-word probe (L1 first: bits set before the level
+//                    are reliable there and RMAT hub words stay hot; a clear
+//                    bit is re-probed at L2), atom.or claim, plain dist store,
+//                    red.or into the next-frontier bitmap (BFS-Hybrid /
+//                    VisitedBitmap)
+//     Winners go to a per-warp shared-memory buffer flushed with one
+//     atomicAdd per <= 512 entries (the GPU form of LocalFrontier +
 //     reserve_and_flush, frontier.hpp:58-98).
 //   bottom-up (kernels.cpp:340-382): warps own 16-word (512-vertex) groups of
-//     the visited bitmap, compact the unvisited ids into shared memory and
-//     scan each one's adjacency until the first frontier-bitmap hit (early
-//     exit). Owner-exclusive: next/visited words are written with plain
-//     stores, no atomics.
+//     the visited bitmap and compact the unvisited ids into shared memory;
+//     each lane probes its vertex's first neighbour (dense first_nbr array,
+//     coalesced) against the frontier bitmap and only on a miss reads rowptr
+//     and scans on in chunks of 8 until the first hit (early exit).
+//     Owner-exclusive: next/visited words are plain stores, no atomics.
 //   control (kernels.cpp:384-464,487-513): distinct size read from the level
 //     counter; `top_down = (double)distinct < thr * (double)n` evaluated in
-//     IEEE double exactly like the reference; representation conversions
-//     (queue <-> bitmap) only when the direction flips.
+//     IEEE double exactly like the reference; bitmap -> queue compaction only
+//     when bottom-up hands over to top-down (top-down winners already marked
+//     the next-frontier bitmap, so the other direction needs no conversion).
 #pragma once
 
 #include <cooperative_groups.h>
