@@ -472,12 +472,28 @@ def run_partitioned(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PBFS_DIST_BACKEND=gloo: collectives staged through host memory and
+    # ranks allowed to share a GPU -- a test mode that runs this exact
+    # multi-process path on a one-GPU box (NCCL refuses two ranks per GPU).
+    backend = os.environ.get("PBFS_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     multi = world > 1
     if multi:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
+
+    def coll(fn, *tensors, **kw):
+        """Run a collective on device tensors (staged through host for gloo)."""
+        if backend == "nccl":
+            return fn(*tensors, **kw)
+        host = [t.cpu() for t in tensors]
+        fn(*host, **kw)
+        for t, h in zip(tensors, host):
+            t.copy_(h)
     G = world if multi else args.partitions
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -509,8 +525,8 @@ def run_partitioned(args):
         else:
             rowptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
             col = torch.empty(m, dtype=torch.int32, device="cuda")
-        tdist.broadcast(rowptr, src=0)
-        tdist.broadcast(col, src=0)
+        coll(tdist.broadcast, rowptr, src=0)
+        coll(tdist.broadcast, col, src=0)
         torch.cuda.synchronize()
         view = dict(vertex_count=n, edge_count=m, row_offsets=rowptr.data_ptr(),
                     column_indices=col.data_ptr(), offset_bytes=8, symmetric=1)
@@ -534,7 +550,10 @@ def run_partitioned(args):
         if multi:
             nxt = parts[0].info()["next"]
             full = torch.as_tensor(_DeviceArray(nxt, wt, "<i4"), device="cuda")
-            tdist.all_gather_into_tensor(full, full[rank * wl:(rank + 1) * wl])
+            if backend == "nccl":
+                tdist.all_gather_into_tensor(full, full[rank * wl:(rank + 1) * wl])
+            else:
+                coll(tdist.all_gather_into_tensor, full, full[rank * wl:(rank + 1) * wl].clone())
 
     def bfs(s):
         for p in parts:
@@ -552,14 +571,14 @@ def run_partitioned(args):
     def reduce_sum(vals):
         if multi:
             t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-            tdist.all_reduce(t)
+            coll(tdist.all_reduce, t)
             return t.tolist()
         return vals
 
     def reduce_max(x):
         if multi:
             t = torch.tensor([x], dtype=torch.float64, device="cuda")
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            coll(tdist.all_reduce, t, op=tdist.ReduceOp.MAX)
             return t.item()
         return x
 
@@ -613,7 +632,7 @@ def run_partitioned(args):
         if multi:
             dl = torch.as_tensor(_DeviceArray(parts[0].info()["dist_local"], nloc, "<i4"),
                                  device="cuda")
-            tdist.all_gather_into_tensor(full_pi, dl)
+            coll(tdist.all_gather_into_tensor, full_pi, dl)
         else:
             for r, p in enumerate(parts):
                 dl = torch.as_tensor(_DeviceArray(p.info()["dist_local"], nloc, "<i4"),
@@ -651,7 +670,7 @@ def run_partitioned(args):
                        "sources": NUM_SOURCES, "source_seed": SOURCE_SEED,
                        "graph_seed": GRAPH_SEED, "variant": "hybrid",
                        "parallelism": (f"1D vertex partition over {world} GPUs, hashed relabel, "
-                                       "per-level NCCL allgather of the frontier bitmap")
+                                       f"per-level {backend} allgather of the frontier bitmap")
                        if multi else f"{G} loopback partitions on one GPU (path test)",
                        "l2": "flushed (512 MiB memset) between traversals",
                        "partition_build_s": round(build_s, 2),
