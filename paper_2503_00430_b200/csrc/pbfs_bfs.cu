@@ -49,6 +49,7 @@ struct pbfs_graph {
   unsigned long long* comp = nullptr;
   uint32_t rec_cap = 0;
   uint64_t qcap = 0, heavy_cap = 0;
+  uint32_t heavy_deg = kHeavyDeg, chunk_log2 = 0;
   int grid = 0;
   size_t bitmap_bytes = 0;
   size_t persist_bytes = 0;  // L2 set-aside granted for the bitmap window
@@ -153,6 +154,8 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.records = g->records;
   p.qcap = g->qcap;
   p.heavy_cap = g->heavy_cap;
+  p.heavy_deg = g->heavy_deg;
+  p.chunk_log2 = g->chunk_log2;
   p.n = g->n;
   p.m = g->m;
   p.max_degree = g->max_degree;
@@ -326,6 +329,11 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   g->words = static_cast<uint32_t>(((n + 31) / 32 + 31) / 32 * 32);
   if (g->words == 0) g->words = kGroupWords;
   std::vector<uint32_t> mask(g->words, 0);
+  const bool big = static_cast<unsigned long long>(g->m) >= kBigArcs;
+  g->heavy_deg = big ? kHeavyDegBig : kHeavyDeg;
+  const uint64_t chunk = big ? kChunkBig : kChunk;
+  static_assert((kChunk & (kChunk - 1)) == 0, "PBFS_CHUNK must be a power of two");
+  while ((1ull << g->chunk_log2) < chunk) ++g->chunk_log2;
   {
     std::vector<uint64_t> mx(threads, 0), hc(threads, 0);
     parallel_for_threads(threads, [&](unsigned t) {
@@ -333,7 +341,7 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
       for (uint64_t v = b; v < en; ++v) {
         const uint64_t d = csr_offset(csr, v + 1) - csr_offset(csr, v);
         mx[t] = std::max(mx[t], d);
-        if (d > kHeavyDeg) hc[t] += (d + kChunk - 1) / kChunk;
+        if (d > g->heavy_deg) hc[t] += (d + chunk - 1) / chunk;
       }
     });
     for (unsigned t = 0; t < threads; ++t) {

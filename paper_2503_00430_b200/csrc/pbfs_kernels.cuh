@@ -58,12 +58,27 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_HEAVY_DEG
 #define PBFS_HEAVY_DEG 128
 #endif
+#ifndef PBFS_PROBE
+// Visited-bit probe of the bitmap claim: 0 = L1 probe, L2 re-probe of clear
+// bits, then the claim atomic; 1 = L2 probe only; 2 = L1 probe straight to
+// the atomic; 3 = the atomic alone (A/B knob). Measured on RMAT-26 (GTEPS,
+// profiles/r01_ab.txt): 0: 367, 1: 398, 2: 411, 3: 167 -- a set bit seen in
+// L1 is final, a clear one is settled by the atomic's returned word, and a
+// separate L2 re-probe costs more round trips than the atomics it saves.
+#define PBFS_PROBE 2
+#endif
 #ifndef PBFS_CHUNK
 #define PBFS_CHUNK 512
 #endif
 constexpr int kMinBlocks = PBFS_MIN_BLOCKS;  // resident CTAs per SM the register budget targets
+// Hub split for graphs below kBigArcs directed arcs; larger graphs take
+// kHeavyDegBig / kChunkBig (their levels are long enough that fewer, larger
+// items beat finer balance). Per graph in Params::heavy_deg / chunk_log2.
 constexpr uint32_t kHeavyDeg = PBFS_HEAVY_DEG;  // degree above which a vertex is split
-constexpr uint32_t kChunk = PBFS_CHUNK;  // edges per heavy work item
+constexpr uint32_t kChunk = PBFS_CHUNK;  // edges per heavy work item (power of two)
+constexpr uint32_t kHeavyDegBig = 2 * PBFS_HEAVY_DEG;
+constexpr uint32_t kChunkBig = 2 * PBFS_CHUNK;
+constexpr unsigned long long kBigArcs = 1ull << 30;
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
 constexpr int kGroupVerts = kGroupWords * 32;
@@ -130,6 +145,8 @@ struct Params {
   unsigned long long max_degree;
   uint32_t words;  // bitmap words, multiple of kGroupWords
   uint32_t rec_cap;
+  uint32_t heavy_deg;   // hub split threshold (kHeavyDeg or kHeavyDegBig)
+  uint32_t chunk_log2;  // log2 of edges per heavy item
   uint32_t source;
   int policy;
   int validate;
@@ -314,6 +331,7 @@ struct WarpTally {
 template <int C, typename OffT>
 __device__ __forceinline__ uint32_t probe_word(const Params<OffT>& p, uint32_t v) {
   if constexpr (C == kClaimBitmap) {
+    if constexpr (PBFS_PROBE == 1) return __ldcg(&p.visited[v >> 5]);
     return __ldca(&p.visited[v >> 5]);
   } else {
     return __ldcg(&p.dist[v]);
@@ -334,7 +352,10 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
   // serialising the round trips this batching exists to overlap.
   uint32_t w[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) w[k] = probe_word<C>(p, v[k]);
+  for (int k = 0; k < K; ++k) {
+    if constexpr (C == kClaimBitmap && PBFS_PROBE == 3) w[k] = 0;
+    else w[k] = probe_word<C>(p, v[k]);
+  }
   if constexpr (C == kClaimPlain) {
     // kernels.cpp:291-301: compare, plain store; racing writers all store the
     // same nd, so duplicates are possible but values are not. Every racing
@@ -355,7 +376,7 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
     (void)wp;
     (void)cnt;
   } else {
-    if constexpr (C == kClaimBitmap) {
+    if constexpr (C == kClaimBitmap && PBFS_PROBE == 0) {
       // Stage 1b: an L1 hit is authoritative for bits set before this level
       // (the grid barrier's fence invalidated L1) -- RMAT hub words stay hot
       // there and never touch the hot L2 slices. A clear bit may be stale
@@ -474,11 +495,12 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
     }
     unsigned long long deg = (unsigned long long)(end - beg);
     t.edges += deg;
-    // Hubs: split into kChunk-edge items for the grid-wide heavy pass; the
+    // Hubs: split into 2^chunk_log2-edge items for the grid-wide heavy pass; the
     // warp reserves all its items with one atomicAdd (a per-vertex atomic on
     // one counter serialises at L2 when a level holds ~1e6 hubs).
-    const bool hub = deg > kHeavyDeg;
-    const unsigned int my_items = hub ? (unsigned int)((deg + kChunk - 1) / kChunk) : 0u;
+    const bool hub = deg > p.heavy_deg;
+    const unsigned long long chunk = 1ull << p.chunk_log2;
+    const unsigned int my_items = hub ? (unsigned int)((deg + chunk - 1) >> p.chunk_log2) : 0u;
     if (__any_sync(FULL, hub)) {
       unsigned int incl = my_items;
 #pragma unroll
@@ -493,8 +515,8 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
       if ((unsigned long long)wbase + wtotal <= p.heavy_cap) {
         const unsigned int slot = wbase + incl - my_items;
         for (unsigned int k = 0; k < my_items; ++k) {
-          const unsigned long long b = (unsigned long long)beg + (unsigned long long)k * kChunk;
-          const unsigned long long e = b + kChunk < (unsigned long long)end ? b + kChunk
+          const unsigned long long b = (unsigned long long)beg + (unsigned long long)k * chunk;
+          const unsigned long long e = b + chunk < (unsigned long long)end ? b + chunk
                                                                             : (unsigned long long)end;
           p.heavy[slot + k] = HeavyItem{b, e};
         }
@@ -545,7 +567,7 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
       }
       claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
     }
-    // Items are equal-sized (kChunk edges but a hub's last one): a static
+    // Items are equal-sized (2^chunk_log2 edges but a hub's last one): a static
     // round-robin balances them without a contended cursor.
     it += warps_total;
   }
@@ -803,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       uint32_t* mark = C == kClaimBitmap ? p.bm[fcur ^ 1] : nullptr;
       uint32_t* stale = C == kClaimBitmap ? p.bm[fcur] : nullptr;
       td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, stale);
-      if (p.max_degree > kHeavyDeg) {
+      if (p.max_degree > p.heavy_deg) {
         bar.sync();
         const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
         if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, mark);

@@ -359,6 +359,8 @@ Params<unsigned long long> td_params(const pbfs_part* g) {
   p.ctl = g->ctl;
   p.qcap = g->nloc + 1;
   p.heavy_cap = g->heavy_cap;
+  p.heavy_deg = kHeavyDeg;
+  p.chunk_log2 = __builtin_ctz(kChunk);
   p.n = g->nloc;
   p.words = (uint32_t)g->lwords;
   p.policy = g->policy;
