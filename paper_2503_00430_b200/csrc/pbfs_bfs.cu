@@ -374,7 +374,8 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   const size_t wbytes = static_cast<size_t>(g->words) * 4;
   if ((st = dalloc(g, &g->rowptr, (n + 1) * offb)) != PBFS_OK) return bail(st);
   // Padded to whole 16 B vectors: hub chunks are read with uint4 loads.
-  if ((st = dalloc(g, &g->col, ((m + 3) / 4) * 16 + 16)) != PBFS_OK) return bail(st);
+  // Whole 64 B windows past the end: bottom-up scans read aligned 16-entry windows.
+  if ((st = dalloc(g, &g->col, ((m + 15) / 16) * 64 + 64)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->init_mask, wbytes)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->first_nbr, (n + 1) * 4)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->dist, ((n + 3) / 4) * 16)) != PBFS_OK) return bail(st);

@@ -67,6 +67,12 @@ constexpr int kWarps = kThreads / 32;
 // separate L2 re-probe costs more round trips than the atomics it saves.
 #define PBFS_PROBE 2
 #endif
+#ifndef PBFS_PRED_TD
+#define PBFS_PRED_TD 1  // predicated-off probes for dead top-down slots (A/B knob)
+#endif
+#ifndef PBFS_PIPE
+#define PBFS_PIPE 0  // software-pipelined hub chunks (A/B knob)
+#endif
 #ifndef PBFS_CHUNK
 #define PBFS_CHUNK 512
 #endif
@@ -80,8 +86,21 @@ constexpr uint32_t kHeavyDegBig = 2 * PBFS_HEAVY_DEG;
 constexpr uint32_t kChunkBig = 2 * PBFS_CHUNK;
 constexpr unsigned long long kBigArcs = 1ull << 30;
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
-constexpr int kGroupWords = 16;      // bottom-up: bitmap words per warp group
-constexpr int kGroupVerts = kGroupWords * 32;
+constexpr int kGroupWords = 32;      // bitmap words per warp group (one per lane)
+constexpr int kListCap = 512;        // bottom-up: unvisited ids listed per round
+#ifndef PBFS_BU_SLOTS
+#define PBFS_BU_SLOTS 4
+#endif
+#ifndef PBFS_BU_GROUPS
+#define PBFS_BU_GROUPS 1
+#endif
+#ifndef PBFS_BU_WIN
+#define PBFS_BU_WIN 8
+#endif
+constexpr int kBuWin = PBFS_BU_WIN;        // bottom-up scan window (8 or 16 entries)
+static_assert(kBuWin == 8 || kBuWin == 16, "PBFS_BU_WIN must be 8 or 16");
+constexpr int kBuSlots = PBFS_BU_SLOTS;    // unvisited vertices per lane in flight
+constexpr int kBuGroups = PBFS_BU_GROUPS;  // 32-word groups per bottom-up task
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
 
 enum Claim : int { kClaimCas = 0, kClaimPlain = 1, kClaimBitmap = 2 };
@@ -99,7 +118,7 @@ struct alignas(128) LevelCnt {
   unsigned int heavy_count;     // heavy items appended
   unsigned int heavy_cursor;    // heavy items grabbed
   unsigned int conv_count;      // bitmap -> queue compaction length
-  unsigned int mark_cursor;
+  unsigned int bu_cursor;       // bottom-up task grab (after the static first)
   unsigned int pad[5];
 };
 
@@ -196,6 +215,15 @@ __device__ __forceinline__ uint32_t ld_cg_if(bool pred, const uint32_t* addr, ui
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
       "@q ld.global.cg.u32 %0, [%2];\n\t}"
+      : "+r"(dflt)
+      : "r"((uint32_t)pred), "l"(addr));
+  return dflt;
+}
+// Predicated L1-allocating load (dead slots issue no request at all).
+__device__ __forceinline__ uint32_t ld_ca_if(bool pred, const uint32_t* addr, uint32_t dflt) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q ld.global.ca.u32 %0, [%2];\n\t}"
       : "+r"(dflt)
       : "r"((uint32_t)pred), "l"(addr));
   return dflt;
@@ -345,8 +373,14 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
   uint32_t w[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    if constexpr (C == kClaimBitmap && PBFS_PROBE == 3) w[k] = 0;
-    else w[k] = probe_word<C>(p, v[k]);
+    if constexpr (C == kClaimBitmap && PBFS_PROBE == 3) {
+      w[k] = 0;
+    } else if constexpr (C == kClaimBitmap && PBFS_PROBE == 2 && PBFS_PRED_TD) {
+      // Dead slots issue no probe (read back as "visited").
+      w[k] = ld_ca_if((okm >> k) & 1u, &p.visited[v[k] >> 5], 0xffffffffu);
+    } else {
+      w[k] = probe_word<C>(p, v[k]);
+    }
   }
   if constexpr (C == kClaimPlain) {
     // kernels.cpp:291-301: compare, plain store; racing writers all store the
@@ -543,6 +577,52 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
   const uint32_t nd = depth + 1;
   const unsigned warps_total = gridDim.x * kWarps;
   unsigned int it = blockIdx.x * kWarps + (threadIdx.x >> 5);
+#if PBFS_PIPE
+  // Software-pipelined: the col loads of batch i+1 (and the header of the
+  // item after next) are issued before batch i's probes and claims, so a
+  // warp keeps two batches of round trips in flight.
+  if (it >= items) return;
+  auto load = [&](const HeavyItem& hh, uint32_t ee, uint32_t (&vv)[K]) -> uint32_t {
+    const uint32_t* b = p.col + hh.beg;
+    const uint32_t ln = (uint32_t)(hh.end - hh.beg);
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t e = ee + 32 * k + lane;
+      const bool ok = e < ln;
+      m |= (uint32_t)ok << k;
+      vv[k] = ld_stream(&b[ok ? e : 0u]);
+    }
+    return m;
+  };
+  HeavyItem h = p.heavy[it];
+  HeavyItem hq = it + warps_total < items ? p.heavy[it + warps_total] : h;
+  uint32_t e0 = 0;
+  uint32_t v[K];
+  uint32_t okm = load(h, 0, v);
+  for (;;) {
+    uint32_t en = e0 + 32 * K;
+    bool more = true;
+    if (en >= (uint32_t)(h.end - h.beg)) {
+      it += warps_total;
+      more = it < items;
+      if (more) {
+        h = hq;
+        if (it + warps_total < items) hq = p.heavy[it + warps_total];
+      }
+      en = 0;
+    }
+    uint32_t vn[K];
+    uint32_t okn = 0;
+    if (more) okn = load(h, en, vn);
+    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
+    if (!more) break;
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = vn[k];
+    okm = okn;
+    e0 = en;
+  }
+#else
   while (it < items) {
     const HeavyItem h = p.heavy[it];
     const uint32_t* base = p.col + h.beg;
@@ -563,121 +643,206 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
     // round-robin balances them without a contended cursor.
     it += warps_total;
   }
+#endif
   (void)FULL;
   (void)cnt;
 }
 
-// Bottom-up over all vertices (kernels.cpp:340-382). Each lane carries KB
-// unvisited vertices at once: the offsets, first neighbours and their
-// frontier words of all KB are loaded before any is resolved; most vertices
-// find a parent at the first probe (RMAT hubs sort first), the rest continue
-// with a serial early-exit scan.
+// Bottom-up over all vertices (kernels.cpp:340-382), per warp task of
+// kBuGroups consecutive 32-word groups (one visited word per lane; all loads
+// of a task in flight together, so settled regions cost a fraction of a
+// round trip per group). Tasks after the first come from a cursor fetched
+// one task ahead. A group's unvisited vertices are listed in shared memory
+// (in rounds of kListCap) and resolved in two stages:
+//  A. kBuSlots per lane at once: the first neighbour (dense first_nbr, a
+//     coalesced read since the list ascends) and its frontier word. On RMAT
+//     nearly every vertex with a frontier parent finds it here (hubs sort
+//     first), without touching rowptr / col.
+//  B. The misses, compacted in place, are scanned in chunks of 8 edges with
+//     lane refill: a lane whose vertex is settled (parent found or list
+//     exhausted) takes the next miss, so the warp is not held to its longest
+//     scan (ER levels scan ~12 edges per vertex with a long geometric tail).
 template <typename OffT>
 __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
-                         uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t) {
-  constexpr int KB = 2;
+                         uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
+                         unsigned int* cursor) {
+  constexpr int KB = kBuSlots;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
   const unsigned warps_total = gridDim.x * kWarps;
   const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t groups = p.words / kGroupWords;
-  for (uint32_t g = gw; g < groups; g += warps_total) {
-    const uint32_t w = g * kGroupWords + (lane & (kGroupWords - 1));
-    const bool owner = lane < (unsigned)kGroupWords;
-    const uint32_t vis = owner ? p.visited[w] : 0xffffffffu;
-    const uint32_t unv = ~vis;
-    const uint32_t c = __popc(unv);
-    uint32_t incl = c;
+  const uint32_t groups = (p.words + 31) / 32;
+  const uint32_t tasks = (groups + kBuGroups - 1) / kBuGroups;
+  const bool beamer = p.policy == kPolicyBeamer;
+  uint32_t task = gw;
+  while (task < tasks) {
+    // Next task index, fetched now so the cursor round trip overlaps this one.
+    uint32_t nxt = 0;
+    if (lane == 0) nxt = warps_total + atomicAdd(cursor, 1u);
+    uint32_t visw[kBuGroups];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(FULL, incl, o);
-      if (lane >= (unsigned)o) incl += x;
+    for (int j = 0; j < kBuGroups; ++j) {
+      const uint32_t w = (task * kBuGroups + j) * 32 + lane;
+      visw[j] = w < p.words ? p.visited[w] : 0xffffffffu;
     }
-    const uint32_t total = __shfl_sync(FULL, incl, 31);
-    if (total == 0) {
-      if (owner) next[w] = 0;
-      continue;
-    }
-    {
-      uint32_t pos = incl - c;
-      uint32_t bits = unv;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        list[pos++] = w * 32 + b;
+#pragma unroll
+    for (int j = 0; j < kBuGroups; ++j) {
+      const uint32_t g = task * kBuGroups + j;
+      if (g >= groups) break;
+      const uint32_t w = g * 32 + lane;
+      const bool owner = w < p.words;
+      const uint32_t vis = visw[j];
+      const uint32_t unv = ~vis;
+      const uint32_t c = __popc(unv);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (unsigned)o) incl += x;
       }
-    }
-    if (owner) found[lane] = 0;
-    __syncwarp();
-    for (uint32_t k = 0; k < total; k += 32 * KB) {
-      uint32_t v[KB], u0[KB], f0[KB];
-      bool valid[KB];
-      // Stage 1: the first neighbour of each vertex from the dense first_nbr
-      // array (coalesced: the list is ascending) and its frontier word. On
-      // RMAT nearly every vertex that has a frontier parent finds it here, so
-      // rowptr / col are not read at all for it. Branch-free loads (dead
-      // slots read list[0]'s data) keep every load of the batch in flight.
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        const uint32_t idx = k + 32 * q + lane;
-        valid[q] = idx < total;
-        v[q] = list[valid[q] ? idx : 0];
-        u0[q] = __ldg(&p.first_nbr[v[q]]);
+      const uint32_t total = __shfl_sync(FULL, incl, 31);
+      if (total == 0) {
+        if (owner) next[w] = 0;
+        continue;
       }
-#pragma unroll
-      for (int q = 0; q < KB; ++q) f0[q] = front[u0[q] >> 5];
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        if (!valid[q]) continue;
-        // kernels.cpp:362-374: first frontier neighbour wins (early exit);
-        // edges count up to and including it.
-        bool hit = (f0[q] >> (u0[q] & 31)) & 1u;
-        unsigned long long scanned = 1;
-        OffT beg = 0, end = 0;
-        if (!hit || p.policy == kPolicyBeamer) {
-          beg = __ldg(&p.rowptr[v[q]]);
-          end = __ldg(&p.rowptr[v[q] + 1]);
+      found[lane] = 0;
+      for (uint32_t r0 = 0; r0 < total; r0 += kListCap) {
+        // This round's slice [r0, r0 + kListCap) of the ascending id list.
+        __syncwarp();
+        {
+          uint32_t pos = incl - c;
+          uint32_t bits = unv;
+          while (bits && pos < r0 + kListCap) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (pos >= r0) list[pos - r0] = w * 32 + b;
+            ++pos;
+          }
         }
-        if (!hit) {
-          // Continue from the second neighbour in chunks of 8: all loads of
-          // a chunk in flight together.
-          for (OffT e0 = beg + 1; !hit && e0 < end; e0 += 8) {
-            uint32_t x[8], fx[8];
+        __syncwarp();
+        const uint32_t cnt = total - r0 < kListCap ? total - r0 : kListCap;
+        // ---- stage A: first neighbours ----
+        uint32_t nmiss = 0;  // warp-uniform; misses compact into list[0, nmiss)
+        for (uint32_t k = 0; k < cnt; k += 32 * KB) {
+          uint32_t v[KB], u0[KB], f0[KB];
+          bool valid[KB];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) x[c] = __ldg(&p.col[e0 + c < end ? e0 + c : e0]);
+          for (int q = 0; q < KB; ++q) {
+            const uint32_t idx = k + 32 * q + lane;
+            valid[q] = idx < cnt;
+            v[q] = list[valid[q] ? idx : 0];
+            u0[q] = __ldg(&p.first_nbr[v[q]]);
+          }
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fx[c] = front[x[c] >> 5];
+          for (int q = 0; q < KB; ++q) f0[q] = front[u0[q] >> 5];
+          __syncwarp();  // every read of list[k, k + 32 KB) precedes the compaction
+#pragma unroll
+          for (int q = 0; q < KB; ++q) {
+            const bool hit = valid[q] && ((f0[q] >> (u0[q] & 31)) & 1u);
+            const bool miss = valid[q] && !hit;
+            if (hit) {
+              // kernels.cpp:362-374: first frontier neighbour wins.
+              p.dist[v[q]] = nd;
+              atomicOr(&found[(v[q] >> 5) - g * 32], 1u << (v[q] & 31));
+              ++t.produced;
+              t.edges += 1;
+              if (beamer) t.degree += (unsigned long long)(__ldg(&p.rowptr[v[q] + 1]) -
+                                                           __ldg(&p.rowptr[v[q]]));
+            }
+            const unsigned mb = __ballot_sync(FULL, miss);
+            if (miss) list[nmiss + __popc(mb & lanemask_lt())] = v[q];
+            nmiss += __popc(mb);
+          }
+        }
+        __syncwarp();
+        // ---- stage B: windowed scans of the misses with lane refill ----
+        // Each lane holds its current vertex plus a prefetched candidate
+        // whose offsets load while the current window is in flight, so a
+        // refill costs no extra round trip.
+        uint32_t pos = 0;  // warp-uniform cursor into list[0, nmiss)
+        bool active = false, cvalid = false;
+        uint32_t v = 0, cv = 0;
+        OffT e = 0, end = 0, beg0 = 0, cbeg = 0, cend = 0;
+        unsigned long long scanned = 0;
+        for (;;) {
+          if (!active && cvalid) {
+            v = cv;
+            beg0 = cbeg;
+            end = cend;
+            e = beg0 + 1;  // the first neighbour was probed in stage A
+            scanned = 1;
+            cvalid = false;
+            active = e < end;
+            if (!active) t.edges += 1;  // degree 1 (isolated vertices are pre-visited)
+          }
+          if (pos < nmiss) {
+            const unsigned need = __ballot_sync(FULL, !cvalid);
+            if (!cvalid) {
+              const uint32_t i = pos + __popc(need & lanemask_lt());
+              if (i < nmiss) {
+                cv = list[i];
+                cbeg = __ldg(&p.rowptr[cv]);
+                cend = __ldg(&p.rowptr[cv + 1]);
+                cvalid = true;
+              }
+            }
+            pos += __popc(need);
+          }
+          if (!__any_sync(FULL, active || cvalid)) break;
+          if (active) {
+            // Aligned kBuWin-entry windows (16 B loads, kBuWin / 8 sectors
+            // per lane); out-of-range slots (other rows, or the allocation's
+            // tail padding) issue no probe -- the probes' L1 tag lookups,
+            // not bytes, bound this loop.
+            const OffT wb = e & ~(OffT)(kBuWin - 1);
+            const uint32_t lo = (uint32_t)(e - wb);
+            const uint32_t hi = end - wb < (OffT)kBuWin ? (uint32_t)(end - wb) : (uint32_t)kBuWin;
+            uint32_t x[kBuWin];
+#pragma unroll
+            for (int q4 = 0; q4 < kBuWin / 4; ++q4) {
+              const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(p.col + wb) + q4);
+              x[4 * q4 + 0] = a4.x;
+              x[4 * q4 + 1] = a4.y;
+              x[4 * q4 + 2] = a4.z;
+              x[4 * q4 + 3] = a4.w;
+            }
+            uint32_t fx[kBuWin];
+#pragma unroll
+            for (int c = 0; c < kBuWin; ++c) {
+              const bool live = (uint32_t)c >= lo && (uint32_t)c < hi;
+              fx[c] = ld_ca_if(live, &front[(live ? x[c] : 0u) >> 5], 0u);
+            }
             unsigned hm = 0;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              hm |= (unsigned)(e0 + c < end && ((fx[c] >> (x[c] & 31)) & 1u)) << c;
-            }
+            for (int c = 0; c < kBuWin; ++c) hm |= ((fx[c] >> (x[c] & 31)) & 1u) << c;
             if (hm) {
-              hit = true;
-              scanned += (unsigned long long)__ffs(hm);
+              scanned += (unsigned long long)(__ffs(hm) - lo);
+              t.edges += scanned;
+              p.dist[v] = nd;
+              atomicOr(&found[(v >> 5) - g * 32], 1u << (v & 31));
+              ++t.produced;
+              if (beamer) t.degree += (unsigned long long)(end - beg0);
+              active = false;
             } else {
-              const OffT rem = end - e0;
-              scanned += rem < 8 ? (unsigned long long)rem : 8ull;
+              scanned += (unsigned long long)(hi - lo);
+              e = wb + kBuWin;
+              if (e >= end) {
+                t.edges += scanned;
+                active = false;
+              }
             }
           }
         }
-        t.edges += scanned;
-        if (hit) {
-          p.dist[v[q]] = nd;
-          atomicOr(&found[(v[q] >> 5) - g * kGroupWords], 1u << (v[q] & 31));
-          ++t.produced;
-          if (p.policy == kPolicyBeamer) t.degree += (unsigned long long)(end - beg);
-        }
+      }
+      __syncwarp();
+      if (owner) {
+        const uint32_t f = found[lane];
+        next[w] = f;
+        if (f) p.visited[w] = vis | f;
       }
     }
-    __syncwarp();
-    if (owner) {
-      const uint32_t f = found[lane];
-      next[w] = f;
-      if (f) p.visited[w] = vis | f;
-    }
-    __syncwarp();
+    task = __shfl_sync(FULL, nxt, 0);
   }
 }
 
@@ -739,7 +904,7 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
 
 template <int C, typename OffT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
-  __shared__ uint32_t s_list[kWarps][kGroupVerts];  // BU id list / TD push buffer
+  __shared__ uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
   __shared__ uint32_t s_found[kWarps][kGroupWords];
   const unsigned warp = threadIdx.x >> 5;
   const unsigned lane = lane_id();
@@ -824,7 +989,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
-      bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t);
+      bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t,
+               &cnt->bu_cursor);
     }
     warp_flush_tally(cnt, t, C == kClaimPlain);
     bar.sync();

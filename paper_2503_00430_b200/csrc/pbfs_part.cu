@@ -236,11 +236,12 @@ __global__ void __launch_bounds__(kThreads) k_td_heavy(Params<OffT> p, uint32_t 
 template <typename OffT>
 __global__ void __launch_bounds__(kThreads) k_bu(Params<OffT> p, uint32_t depth,
                                                  const uint32_t* front, uint32_t* next_local) {
-  __shared__ uint32_t s_list[kWarps][kGroupVerts];
+  __shared__ uint32_t s_list[kWarps][kListCap];
   __shared__ uint32_t s_found[kWarps][kGroupWords];
   const unsigned warp = threadIdx.x >> 5;
   WarpTally t;
-  bu_phase(p, depth, front, next_local, s_list[warp], s_found[warp], t);
+  bu_phase(p, depth, front, next_local, s_list[warp], s_found[warp], t,
+           &p.ctl->cnt[0].bu_cursor);
   warp_flush_tally(&p.ctl->cnt[0], t, false);
 }
 
@@ -407,7 +408,7 @@ pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* co
   PCUDA(cudaStreamSynchronize(s), "partition scan");
   g->m_loc = mloc;
   unsigned long long* colcnt = nullptr;
-  if ((st = palloc(g, &g->colrow, (g->m_loc + 8) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  if ((st = palloc(g, &g->colrow, (g->m_loc + 16) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
   if ((st = palloc(g, &colcnt, (g->npad + 1) * 8)) != PBFS_OK) { cudaFree(tmp); return st; }
   PCUDA(cudaMemsetAsync(colcnt, 0, (g->npad + 1) * 8, s), "memset");
   k_fill_rows<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->rl, g->lo, g->nloc, g->rowloc,
