@@ -40,6 +40,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cstddef>
 #include <cstdint>
 
 #include "pbfs.h"
@@ -69,6 +70,9 @@ constexpr int kWarps = kThreads / 32;
 #endif
 #ifndef PBFS_PRED_TD
 #define PBFS_PRED_TD 1  // predicated-off probes for dead top-down slots (A/B knob)
+#endif
+#ifndef PBFS_TIMELINE
+#define PBFS_TIMELINE 0  // diagnostic per-level timeline in LevelRecord::flush_events
 #endif
 #ifndef PBFS_PIPE
 #define PBFS_PIPE 0  // software-pipelined hub chunks (A/B knob)
@@ -120,6 +124,21 @@ struct alignas(128) LevelCnt {
   unsigned int conv_count;      // bitmap -> queue compaction length
   unsigned int bu_cursor;       // bottom-up task grab (after the static first)
   unsigned int pad[5];
+};
+
+static_assert(offsetof(LevelCnt, degree) == 24 && offsetof(LevelCnt, heavy_count) == 44 &&
+                  offsetof(LevelCnt, conv_count) == 52,
+              "CntSnap offsets");
+
+// Views into a GridBarrier snapshot of a LevelCnt's first 64 bytes.
+struct CntSnap {
+  const unsigned long long* w;
+  __device__ __forceinline__ unsigned long long produced() const { return w[0]; }
+  __device__ __forceinline__ unsigned long long raw() const { return w[1]; }
+  __device__ __forceinline__ unsigned long long edges() const { return w[2]; }
+  __device__ __forceinline__ unsigned long long degree() const { return w[3]; }
+  __device__ __forceinline__ unsigned int heavy_count() const { return (unsigned int)(w[5] >> 32); }
+  __device__ __forceinline__ unsigned int conv_count() const { return (unsigned int)(w[6] >> 32); }
 };
 
 struct alignas(128) Ctl {
@@ -264,7 +283,11 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 // acquire fence follows it.
 struct GridBarrier {
   Ctl* ctl;
-  __device__ __forceinline__ void sync() {
+  unsigned long long* snap;  // shared memory, 8 x u64
+  // `src` (optional, 64 B, 16 B aligned): thread 0 copies it into `snap`
+  // after the barrier, so a CTA reads the level counters with one request
+  // instead of every thread polling the same L2 line.
+  __device__ __forceinline__ void sync(const void* src = nullptr) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
@@ -274,6 +297,12 @@ struct GridBarrier {
       while (((old ^ ld_relaxed(&ctl->bar_word)) & 0x80000000u) == 0) {
       }
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (src) {
+        const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+        const ulonglong2 a = __ldcg(s2), b = __ldcg(s2 + 1), c = __ldcg(s2 + 2), d = __ldcg(s2 + 3);
+        snap[0] = a.x; snap[1] = a.y; snap[2] = b.x; snap[3] = b.y;
+        snap[4] = c.x; snap[5] = c.y; snap[6] = d.x; snap[7] = d.y;
+      }
     }
     __syncthreads();
   }
@@ -846,7 +875,8 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
   }
 }
 
-__device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bool add_raw) {
+__device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bool add_raw,
+                                                 unsigned long long* viol = nullptr) {
   const unsigned FULL = 0xffffffffu;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -861,7 +891,7 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
     if (add_raw && t.raw) atomicAdd(&cnt->raw, t.raw);
     if (t.edges) atomicAdd(&cnt->edges, t.edges);
     if (t.degree) atomicAdd(&cnt->degree, t.degree);
-    if (t.viol) atomicAdd(&cnt->violations, t.viol);
+    if (t.viol) atomicAdd(viol ? viol : &cnt->violations, t.viol);
   }
   t = WarpTally{};
 }
@@ -906,14 +936,18 @@ template <int C, typename OffT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
   __shared__ uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
   __shared__ uint32_t s_found[kWarps][kGroupWords];
+  __shared__ unsigned long long s_snap[8];  // level-counter snapshot (GridBarrier)
   const unsigned warp = threadIdx.x >> 5;
   const unsigned lane = lane_id();
   const unsigned long long tid = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * kThreads;
   Ctl* ctl = p.ctl;
-  GridBarrier bar{ctl};
+  GridBarrier bar{ctl, s_snap};
   WarpPush wp{s_list[warp], 0};
-  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  // Trace records and the end-of-run summary come from the LAST CTA: CTA 0
+  // holds the first frontier slices, the critical path of a small level.
+  const bool leader = blockIdx.x == gridDim.x - 1 && threadIdx.x == 0;
+  const CntSnap snap{s_snap};
 
   // ---- init (Engine ctor + seed, kernels.cpp:72-102,144-163) ------------
   const uint32_t src = p.source;
@@ -939,6 +973,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
         ctl->cnt[s] = z;
       }
       ctl->overflow = 0;
+      ctl->violations = 0;
     }
   }
   const unsigned long long src_deg = degree_of(p, src);
@@ -960,7 +995,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
   int fcur = 0;              // bitmap index holding the current frontier (BU)
   unsigned long long qlen = 1;       // current frontier queue length (raw)
   unsigned long long cur_raw = 1, cur_distinct = 1;
-  unsigned long long reached = 0, edges_total = 0, viol_total = 0;
+  unsigned long long reached = 0, edges_total = 0;
   unsigned int bu_levels = 0;
   unsigned long long t_start = leader ? globaltimer() : 0;
   bar.sync();
@@ -977,38 +1012,61 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       ctl->cnt[(depth + 2) & 3] = z;
     }
     WarpTally t;
+#if PBFS_TIMELINE
+    // Diagnostic build: CTA 0 thread 0's view of the level (it holds the
+    // first frontier slices), packed into the record's flush_events as four
+    // 16-bit ns offsets from the level start.
+    const bool tl_cta = blockIdx.x == 0 && threadIdx.x == 0;
+    const unsigned long long tl0 = tl_cta ? globaltimer() : 0;
+    unsigned long long tl_pack = 0;
+    auto tl_mark = [&](int slot) {
+      if (tl_cta) {
+        const unsigned long long d = globaltimer() - tl0;
+        tl_pack |= (d < 65535 ? d : 65535ull) << (16 * slot);
+        if (slot == 3 && depth < p.rec_cap) p.records[depth].flush_events = tl_pack;
+      }
+    };
+#else
+    auto tl_mark = [](int) {};
+#endif
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
       uint32_t* mark = C == kClaimBitmap ? p.bm[fcur ^ 1] : nullptr;
       uint32_t* stale = C == kClaimBitmap ? p.bm[fcur] : nullptr;
       td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, stale);
+      tl_mark(0);
       if (p.max_degree > p.heavy_deg) {
-        bar.sync();
-        const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
+        bar.sync(cnt);
+        // Bounded by the capacity (an overflow is reported after the run).
+        const unsigned int items = (unsigned long long)snap.heavy_count() < p.heavy_cap
+                                       ? snap.heavy_count()
+                                       : (unsigned int)p.heavy_cap;
         if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, mark);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
       bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t,
                &cnt->bu_cursor);
+      tl_mark(0);
     }
-    warp_flush_tally(cnt, t, C == kClaimPlain);
-    bar.sync();
+    warp_flush_tally(cnt, t, C == kClaimPlain, &ctl->violations);
+    tl_mark(1);
+    bar.sync(cnt);
+    tl_mark(2);
     if constexpr (C == kClaimPlain) {
       // BFS-NonAtomic: the marks collapse into the distinct next frontier.
       compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true);
-      bar.sync();
+      bar.sync(cnt);
     }
     if (C == kClaimBitmap || !td) fcur ^= 1;  // this level's bitmap is the latest
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
     const unsigned long long produced =
-        C == kClaimPlain ? (unsigned long long)*(volatile unsigned int*)&cnt->conv_count
-                         : *(volatile unsigned long long*)&cnt->produced;
-    const unsigned long long raw = td ? *(volatile unsigned long long*)&cnt->raw : produced;
-    const unsigned long long edges = *(volatile unsigned long long*)&cnt->edges;
-    const unsigned long long pdeg = *(volatile unsigned long long*)&cnt->degree;
-    const unsigned int overflow = *(volatile unsigned int*)&ctl->overflow;
+        C == kClaimPlain ? (unsigned long long)snap.conv_count() : snap.produced();
+    const unsigned long long raw = td ? snap.raw() : produced;
+    const unsigned long long edges = snap.edges();
+    const unsigned long long pdeg = snap.degree();
+    tl_mark(3);
     if (leader) {
       const unsigned long long now = globaltimer();
       if (depth < p.rec_cap) {
@@ -1021,20 +1079,32 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
         r.edges_examined = edges;
         r.flush_events = 0;  // no local-buffer flushes to report on the GPU
         r.elapsed_ns = (long long)(now - t_start);
+#if PBFS_TIMELINE
+        pbfs_level* d = &p.records[depth];  // flush_events belongs to CTA 0 here
+        d->depth = r.depth;
+        d->phase = r.phase;
+        d->frontier_size = r.frontier_size;
+        d->distinct_size = r.distinct_size;
+        d->duplicate_count = r.duplicate_count;
+        d->edges_examined = r.edges_examined;
+        d->elapsed_ns = r.elapsed_ns;
+#else
         p.records[depth] = r;
+#endif
       }
       t_start = now;
-      viol_total += *(volatile unsigned long long*)&cnt->violations;
     }
     reached += cur_distinct;
     edges_total += edges;
     bu_levels += td ? 0 : 1;
-    if (overflow || raw == 0) break;
+    if (raw == 0) break;
     unvisited_edges -= pdeg;
     const unsigned long long consumed = cur_distinct;
     const bool next_td = decide(td, produced, pdeg, consumed, unvisited_edges);
     if (td && next_td) {
+      // Bounded by the queue capacity (an overflow is reported after the run).
       qlen = C == kClaimPlain ? produced : raw;
+      if (qlen > p.qcap) qlen = p.qcap;
       qcur ^= 1;
     } else if (!td && next_td) {
       // Entering top-down: ascending queue from the produced bitmap
@@ -1042,8 +1112,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       // stale bitmap is cleared on the way to restore the invariant.
       compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false,
                      p.bm[fcur ^ 1]);
-      bar.sync();
-      qlen = *(volatile unsigned int*)&cnt->conv_count;
+      bar.sync(cnt);
+      qlen = snap.conv_count();
     }
     // top-down -> bottom-up: bm[fcur] already holds the marked frontier;
     // bottom-up -> bottom-up: nothing to convert.
@@ -1057,7 +1127,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     ctl->bu_levels = bu_levels;
     ctl->reached = reached;
     ctl->edges = edges_total;
-    ctl->violations = viol_total;
   }
 }
 
