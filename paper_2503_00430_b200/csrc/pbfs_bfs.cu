@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -50,6 +51,7 @@ struct pbfs_graph {
   uint32_t rec_cap = 0;
   uint64_t qcap = 0, heavy_cap = 0;
   uint32_t heavy_deg = kHeavyDeg, chunk_log2 = 0;
+  uint64_t isolated = 0;  // zero-degree vertices (symmetric graphs), pre-set in init_mask
   int grid = 0;
   size_t bitmap_bytes = 0;
   size_t persist_bytes = 0;  // L2 set-aside granted for the bitmap window
@@ -155,7 +157,9 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.qcap = g->qcap;
   p.heavy_cap = g->heavy_cap;
   p.heavy_deg = g->heavy_deg;
+  p.isolated = g->isolated;
   p.chunk_log2 = g->chunk_log2;
+  p.small_chunks = 1;
   p.n = g->n;
   p.m = g->m;
   p.max_degree = g->max_degree;
@@ -336,21 +340,38 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   while ((1ull << g->chunk_log2) < chunk) ++g->chunk_log2;
   {
     std::vector<uint64_t> mx(threads, 0), hc(threads, 0);
+    std::vector<std::vector<uint64_t>> hubs(threads);
     parallel_for_threads(threads, [&](unsigned t) {
       const uint64_t b = n * t / threads, en = n * (t + 1) / threads;
       for (uint64_t v = b; v < en; ++v) {
         const uint64_t d = csr_offset(csr, v + 1) - csr_offset(csr, v);
         mx[t] = std::max(mx[t], d);
-        if (d > g->heavy_deg) hc[t] += (d + chunk - 1) / chunk;
+        if (d > g->heavy_deg) {
+          hc[t] += (d + chunk - 1) / chunk;
+          hubs[t].push_back(d);
+        }
       }
     });
     for (unsigned t = 0; t < threads; ++t) {
       g->max_degree = std::max(g->max_degree, mx[t]);
       g->heavy_cap += hc[t];
     }
+    // Small frontiers (<= kSmallFrontier vertices) split hubs into
+    // 2^kSmallChunkLog2-edge items so a few hubs still spread over the grid;
+    // their item count is bounded by the kSmallFrontier largest degrees.
+    std::vector<uint64_t> all;
+    for (auto& h : hubs) all.insert(all.end(), h.begin(), h.end());
+    const size_t top = std::min<size_t>(all.size(), kSmallFrontier);
+    std::nth_element(all.begin(), all.begin() + top, all.end(), std::greater<uint64_t>());
+    uint64_t small_items = 0;
+    for (size_t i = 0; i < top; ++i) small_items += (all[i] + (1ull << kSmallChunkLog2) - 1) >> kSmallChunkLog2;
+    g->heavy_cap = std::max(g->heavy_cap, small_items);
     if (g->symmetric) {
       for (uint64_t v = 0; v < n; ++v) {
-        if (csr_offset(csr, v + 1) == csr_offset(csr, v)) mask[v >> 5] |= 1u << (v & 31);
+        if (csr_offset(csr, v + 1) == csr_offset(csr, v)) {
+          mask[v >> 5] |= 1u << (v & 31);
+          ++g->isolated;
+        }
       }
     }
     for (uint64_t v = n; v < static_cast<uint64_t>(g->words) * 32; ++v) mask[v >> 5] |= 1u << (v & 31);

@@ -89,14 +89,21 @@ constexpr uint32_t kChunk = PBFS_CHUNK;  // edges per heavy work item (power of 
 constexpr uint32_t kHeavyDegBig = 2 * PBFS_HEAVY_DEG;
 constexpr uint32_t kChunkBig = 2 * PBFS_CHUNK;
 constexpr unsigned long long kBigArcs = 1ull << 30;
+// Frontiers of at most kSmallFrontier vertices split hubs into 64-edge items:
+// a level with a handful of hubs otherwise keeps only a few hundred warps busy.
+#ifndef PBFS_SMALL_Q
+#define PBFS_SMALL_Q 4096
+#endif
+#ifndef PBFS_SMALL_CHUNK_LOG2
+#define PBFS_SMALL_CHUNK_LOG2 8
+#endif
+constexpr unsigned long long kSmallFrontier = PBFS_SMALL_Q;
+constexpr uint32_t kSmallChunkLog2 = PBFS_SMALL_CHUNK_LOG2;
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 32;      // bitmap words per warp group (one per lane)
 constexpr int kListCap = 512;        // bottom-up: unvisited ids listed per round
 #ifndef PBFS_BU_SLOTS
 #define PBFS_BU_SLOTS 4
-#endif
-#ifndef PBFS_BU_GROUPS
-#define PBFS_BU_GROUPS 1
 #endif
 #ifndef PBFS_BU_WIN
 #define PBFS_BU_WIN 8
@@ -104,7 +111,10 @@ constexpr int kListCap = 512;        // bottom-up: unvisited ids listed per roun
 constexpr int kBuWin = PBFS_BU_WIN;        // bottom-up scan window (8 or 16 entries)
 static_assert(kBuWin == 8 || kBuWin == 16, "PBFS_BU_WIN must be 8 or 16");
 constexpr int kBuSlots = PBFS_BU_SLOTS;    // unvisited vertices per lane in flight
-constexpr int kBuGroups = PBFS_BU_GROUPS;  // 32-word groups per bottom-up task
+// 32-word groups per bottom-up task: 1 (finest balance), or kBuSparseGroups
+// on a sparse level (few unvisited vertices left), where a task is mostly
+// settled words and the round trips, not the scans, are the cost.
+constexpr int kBuSparseGroups = 8;
 constexpr uint32_t kUnreached = 0xFFFFFFFFu;
 
 enum Claim : int { kClaimCas = 0, kClaimPlain = 1, kClaimBitmap = 2 };
@@ -179,8 +189,10 @@ struct Params {
   unsigned long long max_degree;
   uint32_t words;  // bitmap words, multiple of kGroupWords
   uint32_t rec_cap;
+  unsigned long long isolated;  // zero-degree vertices pre-set in init_mask
   uint32_t heavy_deg;   // hub split threshold (kHeavyDeg or kHeavyDegBig)
   uint32_t chunk_log2;  // log2 of edges per heavy item
+  uint32_t small_chunks;  // heavy_cap covers kSmallChunkLog2 items on small frontiers
   uint32_t source;
   int policy;
   int validate;
@@ -554,8 +566,9 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
     // warp reserves all its items with one atomicAdd (a per-vertex atomic on
     // one counter serialises at L2 when a level holds ~1e6 hubs).
     const bool hub = deg > p.heavy_deg;
-    const unsigned long long chunk = 1ull << p.chunk_log2;
-    const unsigned int my_items = hub ? (unsigned int)((deg + chunk - 1) >> p.chunk_log2) : 0u;
+    const uint32_t clog = qlen <= kSmallFrontier && p.small_chunks ? kSmallChunkLog2 : p.chunk_log2;
+    const unsigned long long chunk = 1ull << clog;
+    const unsigned int my_items = hub ? (unsigned int)((deg + chunk - 1) >> clog) : 0u;
     if (__any_sync(FULL, hub)) {
       unsigned int incl = my_items;
 #pragma unroll
@@ -677,10 +690,10 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
   (void)cnt;
 }
 
-// Bottom-up over all vertices (kernels.cpp:340-382), per warp task of
-// kBuGroups consecutive 32-word groups (one visited word per lane; all loads
-// of a task in flight together, so settled regions cost a fraction of a
-// round trip per group). Tasks after the first come from a cursor fetched
+// Bottom-up over all vertices (kernels.cpp:340-382), per warp task of one
+// 32-word group (one visited word per lane), or of kBuSparseGroups groups
+// with all loads in flight when few vertices are left unvisited (settled
+// regions then cost a fraction of a round trip per group). Tasks after the first come from a cursor fetched
 // one task ahead. A group's unvisited vertices are listed in shared memory
 // (in rounds of kListCap) and resolved in two stages:
 //  A. kBuSlots per lane at once: the first neighbour (dense first_nbr, a
@@ -694,7 +707,7 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
 template <typename OffT>
 __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
                          uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
-                         unsigned int* cursor) {
+                         unsigned int* cursor, bool sparse) {
   constexpr int KB = kBuSlots;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -702,26 +715,43 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
   const unsigned warps_total = gridDim.x * kWarps;
   const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint32_t groups = (p.words + 31) / 32;
-  const uint32_t tasks = (groups + kBuGroups - 1) / kBuGroups;
+  const uint32_t gpt = sparse ? (uint32_t)kBuSparseGroups : 1u;
+  const uint32_t tasks = (groups + gpt - 1) / gpt;
   const bool beamer = p.policy == kPolicyBeamer;
   uint32_t task = gw;
   while (task < tasks) {
     // Next task index, fetched now so the cursor round trip overlaps this one.
     uint32_t nxt = 0;
     if (lane == 0) nxt = warps_total + atomicAdd(cursor, 1u);
-    uint32_t visw[kBuGroups];
+    uint32_t visw[kBuSparseGroups];
 #pragma unroll
-    for (int j = 0; j < kBuGroups; ++j) {
-      const uint32_t w = (task * kBuGroups + j) * 32 + lane;
-      visw[j] = w < p.words ? p.visited[w] : 0xffffffffu;
+    for (int j = 0; j < kBuSparseGroups; ++j) {
+      const uint32_t w = (task * gpt + j) * 32 + lane;
+      visw[j] = ((uint32_t)j < gpt && w < p.words) ? p.visited[w] : 0xffffffffu;
     }
+    // Settled groups (no unvisited vertex; padding bits are pre-set) in
+    // bulk, the rest one by one.
+    uint32_t todo = 0;
 #pragma unroll
-    for (int j = 0; j < kBuGroups; ++j) {
-      const uint32_t g = task * kBuGroups + j;
-      if (g >= groups) break;
+    for (int j = 0; j < kBuSparseGroups; ++j) {
+      const uint32_t g = task * gpt + j;
+      if ((uint32_t)j < gpt && g < groups) {
+        if (__any_sync(FULL, visw[j] != 0xffffffffu)) {
+          todo |= 1u << j;
+        } else if (g * 32 + lane < p.words) {
+          next[g * 32 + lane] = 0;
+        }
+      }
+    }
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t g = task * gpt + j;
       const uint32_t w = g * 32 + lane;
       const bool owner = w < p.words;
-      const uint32_t vis = visw[j];
+      uint32_t vis = visw[0];
+#pragma unroll
+      for (int jj = 1; jj < kBuSparseGroups; ++jj) vis = j == jj ? visw[jj] : vis;
       const uint32_t unv = ~vis;
       const uint32_t c = __popc(unv);
       uint32_t incl = c;
@@ -897,20 +927,33 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
 }
 
 // Bitmap -> queue (count_bitmap_slice / write_dense_slice, kernels.cpp:
-// 225-241): each warp compacts 32 words with a popcount scan and reserves its
-// output range with one atomicAdd; optionally clears the words it consumed.
-__device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
-                                               unsigned int* counter, bool clear,
-                                               uint32_t* zero_other = nullptr) {
+// 225-241): each warp takes 8 x 32 words per step (all eight coalesced loads
+// in flight), popcount-scans them and reserves its output range with one
+// atomicAdd; optionally clears the words it consumed and zeroes the same
+// words of a second bitmap. Latency-bound on sparse bitmaps: 8x fewer
+// dependent round trips than one 32-word group per step.
+template <int CW>
+__device__ __forceinline__ void compact_bitmap_cw(uint32_t* nb, uint32_t* q, uint32_t words,
+                                                  unsigned int* counter, bool clear,
+                                                  uint32_t* zero_other) {
   const unsigned lane = lane_id();
   const unsigned warps_total = gridDim.x * kWarps;
   const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  for (uint32_t base = gw * 32; base < words; base += warps_total * 32) {
-    const uint32_t w = base + lane;
-    const uint32_t word = w < words ? nb[w] : 0u;
-    if (clear && word) nb[w] = 0;
-    if (zero_other && w < words) zero_other[w] = 0;
-    const uint32_t c = __popc(word);
+  for (uint32_t base = gw * 32 * CW; base < words; base += warps_total * 32 * CW) {
+    uint32_t wd[CW];
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const uint32_t w = base + 32 * j + lane;
+      wd[j] = w < words ? nb[w] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const uint32_t w = base + 32 * j + lane;
+      if (clear && wd[j]) nb[w] = 0;
+      if (zero_other && w < words) zero_other[w] = 0;
+      c += __popc(wd[j]);
+    }
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -923,12 +966,27 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
     if (lane == 0) off = atomicAdd(counter, total);
     off = __shfl_sync(0xffffffffu, off, 0);
     uint32_t pos = off + incl - c;
-    uint32_t bits = word;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      q[pos++] = w * 32 + b;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      uint32_t bits = wd[j];
+      const uint32_t w = base + 32 * j + lane;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        q[pos++] = w * 32 + b;
+      }
     }
+  }
+}
+// 8 words per lane only when that still gives every warp a step: on small
+// bitmaps one word per lane keeps the bit extraction spread over the grid.
+__device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
+                                               unsigned int* counter, bool clear,
+                                               uint32_t* zero_other = nullptr) {
+  if (words >= gridDim.x * kWarps * 32u * 8u) {
+    compact_bitmap_cw<8>(nb, q, words, counter, clear, zero_other);
+  } else {
+    compact_bitmap_cw<1>(nb, q, words, counter, clear, zero_other);
   }
 }
 
@@ -1045,8 +1103,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
+      // Unvisited non-isolated vertices left (every CTA tracks the same sums).
+      const unsigned long long seen = reached + cur_distinct, live = p.n - p.isolated;
+      const unsigned long long unv = live > seen ? live - seen : 0;
+      // Sparse tasks only where they still give every warp one.
+      const bool sparse =
+          unv * 64 < p.n && p.words >= gridDim.x * kWarps * 32u * (uint32_t)kBuSparseGroups;
       bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t,
-               &cnt->bu_cursor);
+               &cnt->bu_cursor, sparse);
       tl_mark(0);
     }
     warp_flush_tally(cnt, t, C == kClaimPlain, &ctl->violations);

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_bu(Params<OffT> p, uint32_t depth,
   const unsigned warp = threadIdx.x >> 5;
   WarpTally t;
   bu_phase(p, depth, front, next_local, s_list[warp], s_found[warp], t,
-           &p.ctl->cnt[0].bu_cursor);
+           &p.ctl->cnt[0].bu_cursor, false);
   warp_flush_tally(&p.ctl->cnt[0], t, false);
 }
 

@@ -16,6 +16,7 @@ import paper_2503_00430_b200 as pb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="mesh4096")
 ap.add_argument("--sources", type=int, default=2)
+ap.add_argument("--per-level", action="store_true")
 args = ap.parse_args()
 g = bench.build_graph(args.workload)
 cfg, _ = bench.kernel_config(g)
@@ -30,6 +31,12 @@ for s in pb.pick_sources(g, args.sources, 1):
     el = np.array([rec.elapsed_ns for rec in recs], dtype=np.float64)
     print(f"source {s}: {len(recs)} levels, device {r.trace.device_ms:.3f} ms, "
           f"mean level {el.mean()/1e3:.2f} us")
+    if args.per_level:
+        for i, rec in enumerate(recs):
+            mk = " ".join(f"{nm}={marks[i][k]/1e3:.1f}" for k, nm in enumerate(names))
+            print(f"  d={rec.depth:3d} {pb.to_string(rec.phase):9s} frontier={rec.frontier_size:10d} "
+                  f"edges={rec.edges_examined:12d} span={el[i]/1e3:8.1f} us | {mk}")
+        continue
     sel = slice(2, len(recs) - 1)
     m = marks[sel].mean(axis=0)
     prev = 0.0
