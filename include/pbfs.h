@@ -165,6 +165,18 @@ pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
                      uint32_t* dist_host, pbfs_level* levels, uint32_t levels_cap,
                      pbfs_run_info* info);
 
+/* A batch of traversals (the reference's per-source loop in time_run /
+ * bfsbench run, timing.cpp:74-76, bfsbench.cpp:458-460) with the distance
+ * array of source i copied to dist_host[i] while source i+1 traverses: two
+ * device distance buffers, the copies on a second stream. dist_host[i] may
+ * repeat (e.g. two rotating buffers); it should be pinned (pbfs_host_alloc)
+ * for the copies to overlap. infos: NULL or `count` entries (device_ms is the
+ * traversal alone). Same checks and errors as pbfs_bfs, for every source
+ * before any launch. Synchronous: returns when every copy has landed. */
+pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t count,
+                           const pbfs_config* cfg, uint32_t* const* dist_host,
+                           pbfs_run_info* infos);
+
 /* Enqueue-only traversal on a caller stream (cudaStream_t passed as void*,
  * NULL = the handle's stream); distances stay in HBM. No trace, no host sync.
  * For benchmark loops that keep inputs resident. pbfs_graph_sync() collects

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("pbfs_graph_destroy", ctypes.c_int, [c_vp]),
     ("pbfs_graph_get_info", ctypes.c_int, [c_vp, P(GraphInfo)]),
     ("pbfs_bfs", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp, P(Level), c_u32, P(RunInfo)]),
+    ("pbfs_bfs_batch", ctypes.c_int, [c_vp, P(c_u32), c_u32, P(Config), P(c_vp), P(RunInfo)]),
     ("pbfs_bfs_async", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),
     ("pbfs_graph_sync", ctypes.c_int, [c_vp, c_vp]),
     ("pbfs_graph_device_dist", ctypes.c_int, [c_vp, P(c_vp)]),

@@ -58,6 +58,14 @@ struct pbfs_graph {
   uint64_t device_bytes = 0;
   std::vector<void*> allocs;
   bool poisoned = false;  // a launch failed; ctl must be reset
+  // pbfs_bfs_batch state, created on first use.
+  uint32_t* dist2 = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t kern_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+  cudaEvent_t bev[2] = {nullptr, nullptr};
+  Ctl* ctl_host = nullptr;  // pinned, ctl_host_cap entries
+  uint32_t ctl_host_cap = 0;
+  std::vector<cudaEvent_t> run_ev;  // per-source start/end events (2 per source)
 };
 
 namespace {
@@ -94,6 +102,13 @@ void release(pbfs_graph* g) {
   cudaGetDevice(&prev);
   cudaSetDevice(g->device);
   for (void* p : g->allocs) cudaFree(p);
+  if (g->ctl_host) cudaFreeHost(g->ctl_host);
+  for (cudaEvent_t e : g->run_ev) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (g->kern_done[i]) cudaEventDestroy(g->kern_done[i]);
+    if (g->copy_done[i]) cudaEventDestroy(g->copy_done[i]);
+  }
+  if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
@@ -139,11 +154,11 @@ pbfs_status map_variant(const pbfs_config* c, bool* hybrid_like, Launch* out) {
 
 template <int C, typename OffT>
 cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, int policy,
-                         cudaStream_t s) {
+                         cudaStream_t s, uint32_t* dist) {
   Params<OffT> p;
   p.rowptr = static_cast<const OffT*>(g->rowptr);
   p.col = g->col;
-  p.dist = g->dist;
+  p.dist = dist;
   p.visited = g->visited;
   p.bm[0] = g->bm[0];
   p.bm[1] = g->bm[1];
@@ -196,18 +211,19 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
 }
 
 cudaError_t launch(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, const Launch& l,
-                   cudaStream_t s) {
+                   cudaStream_t s, uint32_t* dist = nullptr) {
   const bool wide = g->offb == 8;
+  if (!dist) dist = g->dist;
   switch (l.claim) {
     case kClaimCas:
-      return wide ? launch_typed<kClaimCas, unsigned long long>(g, source, cfg, l.policy, s)
-                  : launch_typed<kClaimCas, uint32_t>(g, source, cfg, l.policy, s);
+      return wide ? launch_typed<kClaimCas, unsigned long long>(g, source, cfg, l.policy, s, dist)
+                  : launch_typed<kClaimCas, uint32_t>(g, source, cfg, l.policy, s, dist);
     case kClaimPlain:
-      return wide ? launch_typed<kClaimPlain, unsigned long long>(g, source, cfg, l.policy, s)
-                  : launch_typed<kClaimPlain, uint32_t>(g, source, cfg, l.policy, s);
+      return wide ? launch_typed<kClaimPlain, unsigned long long>(g, source, cfg, l.policy, s, dist)
+                  : launch_typed<kClaimPlain, uint32_t>(g, source, cfg, l.policy, s, dist);
     default:
-      return wide ? launch_typed<kClaimBitmap, unsigned long long>(g, source, cfg, l.policy, s)
-                  : launch_typed<kClaimBitmap, uint32_t>(g, source, cfg, l.policy, s);
+      return wide ? launch_typed<kClaimBitmap, unsigned long long>(g, source, cfg, l.policy, s, dist)
+                  : launch_typed<kClaimBitmap, uint32_t>(g, source, cfg, l.policy, s, dist);
   }
 }
 
@@ -548,6 +564,94 @@ pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uin
   }
   if (ctl.levels > g->rec_cap && levels) {
     return fail(PBFS_E_CAPACITY, "traversal depth exceeds the device trace capacity");
+  }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t count,
+                           const pbfs_config* cfg, uint32_t* const* dist_host,
+                           pbfs_run_info* infos) {
+  if (!g) return fail(PBFS_E_INPUT, "null graph");
+  if (count && (!sources || !dist_host)) return fail(PBFS_E_INPUT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  Launch l;
+  for (uint32_t i = 0; i < count; ++i) {
+    pbfs_status st = prologue(g, sources[i], cfg, &l);
+    if (st != PBFS_OK) return st;
+  }
+  if (count == 0) return PBFS_OK;
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaError_t e;
+  if (!g->copy_stream) {
+    PBFS_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+      PBFS_CUDA(cudaEventCreateWithFlags(&g->kern_done[i], cudaEventDisableTiming), "cudaEventCreate");
+      PBFS_CUDA(cudaEventCreateWithFlags(&g->copy_done[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  if (!g->dist2) {
+    pbfs_status st = dalloc(g, &g->dist2, g->n * 4 + 16);
+    if (st != PBFS_OK) return st;
+  }
+  if (g->ctl_host_cap < count) {
+    if (g->ctl_host) cudaFreeHost(g->ctl_host);
+    g->ctl_host = nullptr;
+    g->ctl_host_cap = 0;
+    PBFS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->ctl_host), count * sizeof(Ctl),
+                            cudaHostAllocDefault), "pinned control snapshots");
+    g->ctl_host_cap = count;
+  }
+  while (g->run_ev.size() < 2ull * count) {
+    cudaEvent_t ev;
+    PBFS_CUDA(cudaEventCreate(&ev), "cudaEventCreate");
+    g->run_ev.push_back(ev);
+  }
+  uint32_t* buf[2] = {g->dist, g->dist2};
+  for (uint32_t i = 0; i < count; ++i) {
+    const int slot = i & 1;
+    // The buffer of source i-2 must have reached the host before reuse.
+    if (i >= 2) PBFS_CUDA(cudaStreamWaitEvent(g->stream, g->copy_done[slot], 0), "stream wait");
+    PBFS_CUDA(cudaEventRecord(g->run_ev[2 * i], g->stream), "event record");
+    if ((e = launch(g, sources[i], cfg, l, g->stream, buf[slot])) != cudaSuccess) {
+      g->poisoned = true;
+      cudaStreamSynchronize(g->copy_stream);
+      return cuda_fail(e, "traversal launch");
+    }
+    PBFS_CUDA(cudaEventRecord(g->run_ev[2 * i + 1], g->stream), "event record");
+    PBFS_CUDA(cudaMemcpyAsync(&g->ctl_host[i], g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                              g->stream), "read control");
+    PBFS_CUDA(cudaEventRecord(g->kern_done[slot], g->stream), "event record");
+    PBFS_CUDA(cudaStreamWaitEvent(g->copy_stream, g->kern_done[slot], 0), "stream wait");
+    PBFS_CUDA(cudaMemcpyAsync(dist_host[i], buf[slot], g->n * 4, cudaMemcpyDeviceToHost,
+                              g->copy_stream), "read distances");
+    PBFS_CUDA(cudaEventRecord(g->copy_done[slot], g->copy_stream), "event record");
+  }
+  cudaError_t e1 = cudaStreamSynchronize(g->stream);
+  cudaError_t e2 = cudaStreamSynchronize(g->copy_stream);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    g->poisoned = true;
+    return cuda_fail(e1 != cudaSuccess ? e1 : e2, "traversal batch");
+  }
+  // The handle's dist keeps meaning "the last traversal" (device_dist, component).
+  if ((count - 1) & 1) std::swap(g->dist, g->dist2);
+  for (uint32_t i = 0; i < count; ++i) {
+    const Ctl& c = g->ctl_host[i];
+    if (c.overflow) {
+      g->poisoned = true;
+      return fail(PBFS_E_CAPACITY, "dense frontier overflow");
+    }
+    if (infos) {
+      pbfs_run_info* info = &infos[i];
+      std::memset(info, 0, sizeof(*info));
+      info->levels = c.levels;
+      info->bottom_up_levels = c.bu_levels;
+      info->reached = c.reached;
+      info->same_value_violations = c.violations;
+      info->edges_examined = c.edges;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, g->run_ev[2 * i], g->run_ev[2 * i + 1]);
+      info->device_ms = ms;
+    }
   }
   return PBFS_OK;
 }

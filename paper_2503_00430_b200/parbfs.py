@@ -26,7 +26,7 @@ import enum
 import time
 import weakref
 from dataclasses import dataclass, field
-from typing import Callable, Optional
+from typing import Callable, List, Optional
 
 import numpy as np
 
@@ -550,6 +550,24 @@ class DeviceGraph:
                                                  r.distinct_size, r.duplicate_count,
                                                  r.edges_examined, r.flush_events, r.elapsed_ns))
         return BfsResult(dist, trace)
+
+    def bfs_batch(self, sources, config: KernelConfig, outs) -> List[float]:
+        """pbfs_bfs_batch: traversal i+1 overlaps the host copy of distances i.
+        `outs[i]` receives source i's distances (entries may repeat, e.g. two
+        rotating pinned buffers). Returns per-source device ms."""
+        srcs = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
+        k = int(srcs.size)
+        if len(outs) != k:
+            raise ConfigError("bfs_batch needs one output buffer per source")
+        for o in outs:
+            if o.dtype != np.uint32 or o.size != self.vertex_count or not o.flags.c_contiguous:
+                raise ConfigError("bfs_batch outputs must be contiguous uint32[vertex_count]")
+        c = config._c()
+        ptrs = (ctypes.c_void_p * k)(*[o.ctypes.data for o in outs])
+        infos = (L.RunInfo * k)()
+        _check(lib.pbfs_bfs_batch(self.h, srcs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                  k, ctypes.byref(c), ptrs, infos))
+        return [float(infos[i].device_ms) for i in range(k)]
 
     def bfs_async(self, source: int, config: KernelConfig, stream: int = 0) -> None:
         c = config._c()

@@ -279,6 +279,35 @@ def test_async_api_and_device_component(port):
     assert (nr, ar) == port.component(g.row_offsets, want)
 
 
+def test_batch_api_overlapped_copies(port):
+    # pbfs_bfs_batch: distances of source i land in outs[i] while i+1 runs.
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 3,
+                                     drop_self_loops=True))
+    dg = g.device(0, 8)
+    srcs = [int(s) for s in pb.pick_sources(g, 7, 4)]
+    want = {s: port.bfs_serial(g.row_offsets, g.column_indices, s) for s in srcs}
+    for v in (V.Hybrid, V.Conventional, V.NonAtomic):
+        cfg = pb.KernelConfig(variant=v)
+        outs = [pb.parbfs.pinned_empty(g.vertex_count, np.uint32) for _ in srcs]
+        ms = dg.bfs_batch(srcs, cfg, outs)
+        assert len(ms) == len(srcs) and all(t > 0 for t in ms)
+        for s, o in zip(srcs, outs):
+            assert np.array_equal(o, want[s])
+        # the handle's device distances are the last source's
+        nr, ar = dg.component()
+        assert (nr, ar) == port.component(g.row_offsets, want[srcs[-1]])
+        # two rotating buffers: each ends with the last source written to it
+        rot = [pb.parbfs.pinned_empty(g.vertex_count, np.uint32) for _ in range(2)]
+        dg.bfs_batch(srcs, cfg, [rot[i % 2] for i in range(len(srcs))])
+        assert np.array_equal(rot[(len(srcs) - 1) % 2], want[srcs[-1]])
+        assert np.array_equal(rot[(len(srcs) - 2) % 2], want[srcs[-2]])
+        # a single traversal after a batch still sees the right buffers
+        assert np.array_equal(dg.bfs(srcs[0], cfg).distances, want[srcs[0]])
+    with pytest.raises(pb.InputError, match="out of range"):
+        dg.bfs_batch([0, g.vertex_count], pb.KernelConfig(variant=V.Hybrid),
+                     [np.empty(g.vertex_count, np.uint32)] * 2)
+
+
 def test_time_run_checks_every_run(port):
     # timing.cpp:33-69 and test_instrumentation.cpp:168-198 (fault injection)
     g = make_circulant(64, [3])
