@@ -271,7 +271,8 @@ bool is_symmetric(const HostCsr& g, unsigned threads) {
 //   3. per bucket: sort + unique + per-row degree, dst compacted in place,
 //   4. offsets by prefix sum, columns copied out bucket by bucket.
 pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, bool symmetrize,
-                           bool drop_self_loops, unsigned threads, HostCsr* out) {
+                           bool drop_self_loops, unsigned threads, HostCsr* out,
+                           std::unique_ptr<uint32_t[]>* owned_pairs = nullptr) {
   if (n > 0x7fffffffULL) {
     return fail(PBFS_E_INPUT, "vertex count " + std::to_string(n) +
                                   " exceeds the supported maximum 2147483647");
@@ -329,7 +330,8 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
     bucket_start[nbuckets] = run;
   }
   const uint64_t total = bucket_start[nbuckets];
-  std::unique_ptr<uint64_t[]> keys(new (std::nothrow) uint64_t[total ? total : 1]);
+  std::unique_ptr<uint64_t[], FreeDeleter> keys(
+      static_cast<uint64_t*>(std::malloc((total ? total : 1) * sizeof(uint64_t))));
   if (!keys) return fail(PBFS_E_CAPACITY, "host allocation failed for " + std::to_string(total) + " arcs");
   parallel_for_threads(threads, [&](unsigned t) {
     uint64_t* pos = hist.data() + t * nbuckets;
@@ -346,6 +348,8 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
   });
   hist.clear();
   hist.shrink_to_fit();
+  // Peak host memory at RMAT-28 is pairs + keys; the pairs are dead from here.
+  if (owned_pairs) owned_pairs->reset();
 
   out->n = n;
   out->offsets.reset(new (std::nothrow) uint64_t[n + 1]);
@@ -380,8 +384,6 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
   for (uint64_t bk = 0; bk < nbuckets; ++bk) bucket_base[bk + 1] = bucket_base[bk] + bucket_unique[bk];
   const uint64_t m = bucket_base[nbuckets];
   out->m = m;
-  out->col.reset(new (std::nothrow) uint32_t[m ? m : 1]);
-  if (!out->col) return fail(PBFS_E_CAPACITY, "host allocation failed (columns)");
   out->offsets[0] = 0;
   next_bucket = 0;
   parallel_for_threads(threads, [&](unsigned) {
@@ -394,11 +396,19 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
         run += out->offsets[v + 1];
         out->offsets[v + 1] = run;
       }
-      std::memcpy(out->col.get() + bucket_base[bk], colbuf + 2 * bucket_start[bk],
-                  bucket_unique[bk] * sizeof(uint32_t));
     }
   });
-  keys.reset();
+  // Columns: slide every bucket's compacted u32 run to its final position in
+  // the same buffer (destinations never pass the sources: bucket_base[bk] <=
+  // 2 * bucket_start[bk], and buckets move in ascending order), then shrink.
+  for (uint64_t bk = 0; bk < nbuckets; ++bk) {
+    std::memmove(colbuf + bucket_base[bk], colbuf + 2 * bucket_start[bk],
+                 bucket_unique[bk] * sizeof(uint32_t));
+  }
+  void* shrunk = std::realloc(keys.get(), (m ? m : 1) * sizeof(uint32_t));
+  if (!shrunk) return fail(PBFS_E_CAPACITY, "host reallocation failed (columns)");
+  keys.release();
+  out->col.reset(static_cast<uint32_t*>(shrunk));
   out->symmetric = symmetrize ? true : is_symmetric(*out, threads);
   return PBFS_OK;
 }
@@ -472,6 +482,22 @@ pbfs_status pbfs_build_csr(const uint32_t* pairs, uint64_t npairs, uint64_t vert
   return PBFS_OK;
 }
 
+// pbfs_build_csr over generator-owned pairs, which the builder frees as soon
+// as it has scattered them.
+static pbfs_status build_to_handle(const uint32_t* pairs, uint64_t npairs, uint64_t n,
+                                   uint32_t drop_self_loops, unsigned threads, pbfs_host_csr** out,
+                                   std::unique_ptr<uint32_t[]>* owned) {
+  auto* h = new (std::nothrow) pbfs_host_csr;
+  if (!h) return fail(PBFS_E_CAPACITY, "host allocation failed");
+  pbfs_status st = build_csr_impl(pairs, npairs, n, true, drop_self_loops != 0, threads, &h->g, owned);
+  if (st != PBFS_OK) {
+    delete h;
+    return st;
+  }
+  *out = h;
+  return PBFS_OK;
+}
+
 pbfs_status pbfs_generate(const pbfs_gen_spec* spec, pbfs_host_csr** out) {
   if (!spec || !out) return fail(PBFS_E_INPUT, "null argument");
   const unsigned threads = resolve_threads(spec->threads);
@@ -502,7 +528,7 @@ pbfs_status pbfs_generate(const pbfs_gen_spec* spec, pbfs_host_csr** out) {
       return fail(PBFS_E_CAPACITY, "host allocation failed for " + std::to_string(samples) + " samples");
     }
     sample_pairs(spec->kind, spec->scale, spec->edge_factor, spec->seed, threads, raw.get());
-    return pbfs_build_csr(raw.get(), samples, n, 1, spec->drop_self_loops, threads, out);
+    return build_to_handle(raw.get(), samples, n, spec->drop_self_loops, threads, out, &raw);
   } else {
     return fail(PBFS_E_CONFIG, "unknown generator kind");
   }
@@ -603,7 +629,7 @@ pbfs_status pbfs_load_csr1(const char* path, pbfs_host_csr** out) {
   h->g.n = n;
   h->g.m = m;
   h->g.offsets.reset(new (std::nothrow) uint64_t[n + 1]);
-  h->g.col.reset(new (std::nothrow) uint32_t[m ? m : 1]);
+  h->g.col.reset(static_cast<uint32_t*>(std::malloc((m ? m : 1) * sizeof(uint32_t))));
   if (!h->g.offsets || !h->g.col) {
     std::fclose(f);
     delete h;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <thread>
@@ -18,11 +19,17 @@ void clear_error();
 
 // Host CSR owned by the library. Raw arrays (no value-initialisation) so a
 // multi-GB graph is not zero-filled before the builder overwrites it.
+struct FreeDeleter {
+  void operator()(void* p) const { std::free(p); }
+};
+
 struct HostCsr {
   uint64_t n = 0;
   uint64_t m = 0;
   std::unique_ptr<uint64_t[]> offsets;  // n + 1
-  std::unique_ptr<uint32_t[]> col;      // m
+  // malloc'd: the builder compacts the columns inside its key buffer and
+  // shrinks it with realloc instead of holding a second m-sized array.
+  std::unique_ptr<uint32_t[], FreeDeleter> col;  // m
   bool symmetric = false;
 };
 
