@@ -484,6 +484,16 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   const char* no_persist = std::getenv("PBFS_NO_L2_PERSIST");
   if (prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0 &&
       !(no_persist && no_persist[0] == '1')) {
+    // The window covers all three bitmaps when they fit the set-aside; else
+    // only `visited` (the top-down probe target): a window larger than the
+    // set-aside thrashes its own lines (RMAT-28: 96 MB of bitmaps, 79 MB
+    // set-aside). PBFS_L2_WINDOW=all|visited overrides for A/B runs.
+    const char* win = std::getenv("PBFS_L2_WINDOW");
+    const size_t vis_bytes = static_cast<size_t>(g->words) * 4;
+    bool all = g->bitmap_bytes <= static_cast<size_t>(prop.persistingL2CacheMaxSize);
+    if (win && std::strcmp(win, "all") == 0) all = true;
+    if (win && std::strcmp(win, "visited") == 0) all = false;
+    if (!all) g->bitmap_bytes = vis_bytes;
     g->bitmap_bytes = std::min<size_t>(g->bitmap_bytes, prop.accessPolicyMaxWindowSize);
     const size_t want = std::min<size_t>(g->bitmap_bytes, prop.persistingL2CacheMaxSize);
     size_t cur = 0;
