@@ -52,6 +52,7 @@ struct pbfs_graph {
   uint64_t qcap = 0, heavy_cap = 0;
   uint32_t heavy_deg = kHeavyDeg, chunk_log2 = 0;
   uint64_t isolated = 0;  // zero-degree vertices (symmetric graphs), pre-set in init_mask
+  uint32_t force = 0;     // kForce* test hooks
   int grid = 0;
   size_t bitmap_bytes = 0;
   size_t persist_bytes = 0;  // L2 set-aside granted for the bitmap window
@@ -175,6 +176,7 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.isolated = g->isolated;
   p.chunk_log2 = g->chunk_log2;
   p.small_chunks = 1;
+  p.force = g->force;
   p.n = g->n;
   p.m = g->m;
   p.max_degree = g->max_degree;
@@ -349,7 +351,10 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   g->words = static_cast<uint32_t>(((n + 31) / 32 + 31) / 32 * 32);
   if (g->words == 0) g->words = kGroupWords;
   std::vector<uint32_t> mask(g->words, 0);
-  const bool big = static_cast<unsigned long long>(g->m) >= kBigArcs;
+  // PBFS_FORCE_MODES (test hook, a kForce* bitmask) forces the size-gated
+  // paths on any graph so small-graph parity tests cover them.
+  if (const char* fm = std::getenv("PBFS_FORCE_MODES")) g->force = static_cast<uint32_t>(std::strtoul(fm, nullptr, 0));
+  const bool big = static_cast<unsigned long long>(g->m) >= kBigArcs || (g->force & kForceBigSplit);
   g->heavy_deg = big ? kHeavyDegBig : kHeavyDeg;
   const uint64_t chunk = big ? kChunkBig : kChunk;
   static_assert((kChunk & (kChunk - 1)) == 0, "PBFS_CHUNK must be a power of two");

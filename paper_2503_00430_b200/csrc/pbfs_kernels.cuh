@@ -74,9 +74,6 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_TIMELINE
 #define PBFS_TIMELINE 0  // diagnostic per-level timeline in LevelRecord::flush_events
 #endif
-#ifndef PBFS_PIPE
-#define PBFS_PIPE 0  // software-pipelined hub chunks (A/B knob)
-#endif
 #ifndef PBFS_CHUNK
 #define PBFS_CHUNK 512
 #endif
@@ -98,6 +95,10 @@ constexpr unsigned long long kBigArcs = 1ull << 30;
 #define PBFS_SMALL_CHUNK_LOG2 8
 #endif
 constexpr unsigned long long kSmallFrontier = PBFS_SMALL_Q;
+// Test hooks: run the size-gated paths on small graphs (parity coverage).
+constexpr uint32_t kForceSparseBu = 1;     // sparse bottom-up tasks at every level
+constexpr uint32_t kForceWideCompact = 2;  // 8-words-per-lane compaction
+constexpr uint32_t kForceBigSplit = 4;     // the >= 2^30-arc hub split
 constexpr uint32_t kSmallChunkLog2 = PBFS_SMALL_CHUNK_LOG2;
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 32;      // bitmap words per warp group (one per lane)
@@ -193,6 +194,7 @@ struct Params {
   uint32_t heavy_deg;   // hub split threshold (kHeavyDeg or kHeavyDegBig)
   uint32_t chunk_log2;  // log2 of edges per heavy item
   uint32_t small_chunks;  // heavy_cap covers kSmallChunkLog2 items on small frontiers
+  uint32_t force;         // kForce* test hooks (PBFS_FORCE_MODES at graph creation)
   uint32_t source;
   int policy;
   int validate;
@@ -619,52 +621,6 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
   const uint32_t nd = depth + 1;
   const unsigned warps_total = gridDim.x * kWarps;
   unsigned int it = blockIdx.x * kWarps + (threadIdx.x >> 5);
-#if PBFS_PIPE
-  // Software-pipelined: the col loads of batch i+1 (and the header of the
-  // item after next) are issued before batch i's probes and claims, so a
-  // warp keeps two batches of round trips in flight.
-  if (it >= items) return;
-  auto load = [&](const HeavyItem& hh, uint32_t ee, uint32_t (&vv)[K]) -> uint32_t {
-    const uint32_t* b = p.col + hh.beg;
-    const uint32_t ln = (uint32_t)(hh.end - hh.beg);
-    uint32_t m = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t e = ee + 32 * k + lane;
-      const bool ok = e < ln;
-      m |= (uint32_t)ok << k;
-      vv[k] = ld_stream(&b[ok ? e : 0u]);
-    }
-    return m;
-  };
-  HeavyItem h = p.heavy[it];
-  HeavyItem hq = it + warps_total < items ? p.heavy[it + warps_total] : h;
-  uint32_t e0 = 0;
-  uint32_t v[K];
-  uint32_t okm = load(h, 0, v);
-  for (;;) {
-    uint32_t en = e0 + 32 * K;
-    bool more = true;
-    if (en >= (uint32_t)(h.end - h.beg)) {
-      it += warps_total;
-      more = it < items;
-      if (more) {
-        h = hq;
-        if (it + warps_total < items) hq = p.heavy[it + warps_total];
-      }
-      en = 0;
-    }
-    uint32_t vn[K];
-    uint32_t okn = 0;
-    if (more) okn = load(h, en, vn);
-    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
-    if (!more) break;
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = vn[k];
-    okm = okn;
-    e0 = en;
-  }
-#else
   while (it < items) {
     const HeavyItem h = p.heavy[it];
     const uint32_t* base = p.col + h.beg;
@@ -685,7 +641,6 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
     // round-robin balances them without a contended cursor.
     it += warps_total;
   }
-#endif
   (void)FULL;
   (void)cnt;
 }
@@ -982,8 +937,8 @@ __device__ __forceinline__ void compact_bitmap_cw(uint32_t* nb, uint32_t* q, uin
 // bitmaps one word per lane keeps the bit extraction spread over the grid.
 __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
                                                unsigned int* counter, bool clear,
-                                               uint32_t* zero_other = nullptr) {
-  if (words >= gridDim.x * kWarps * 32u * 8u) {
+                                               uint32_t* zero_other = nullptr, bool wide = false) {
+  if (wide || words >= gridDim.x * kWarps * 32u * 8u) {
     compact_bitmap_cw<8>(nb, q, words, counter, clear, zero_other);
   } else {
     compact_bitmap_cw<1>(nb, q, words, counter, clear, zero_other);
@@ -1108,7 +1063,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       const unsigned long long unv = live > seen ? live - seen : 0;
       // Sparse tasks only where they still give every warp one.
       const bool sparse =
-          unv * 64 < p.n && p.words >= gridDim.x * kWarps * 32u * (uint32_t)kBuSparseGroups;
+          (p.force & kForceSparseBu) ||
+          (unv * 64 < p.n && p.words >= gridDim.x * kWarps * 32u * (uint32_t)kBuSparseGroups);
       bu_phase(p, depth, p.bm[fcur], p.bm[fcur ^ 1], s_list[warp], s_found[warp], t,
                &cnt->bu_cursor, sparse);
       tl_mark(0);
@@ -1119,7 +1075,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     tl_mark(2);
     if constexpr (C == kClaimPlain) {
       // BFS-NonAtomic: the marks collapse into the distinct next frontier.
-      compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true);
+      compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true, nullptr,
+                     p.force & kForceWideCompact);
       bar.sync(cnt);
     }
     if (C == kClaimBitmap || !td) fcur ^= 1;  // this level's bitmap is the latest
@@ -1175,7 +1132,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241); the
       // stale bitmap is cleared on the way to restore the invariant.
       compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false,
-                     p.bm[fcur ^ 1]);
+                     p.bm[fcur ^ 1], p.force & kForceWideCompact);
       bar.sync(cnt);
       qlen = snap.conv_count();
     }

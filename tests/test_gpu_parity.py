@@ -308,6 +308,29 @@ def test_batch_api_overlapped_copies(port):
                      [np.empty(g.vertex_count, np.uint32)] * 2)
 
 
+@pytest.mark.parametrize("force", [1, 2, 4, 7])
+def test_size_gated_paths_forced_on_small_graphs(force, port, monkeypatch):
+    # Paths that only switch on at RMAT-26 scale (sparse bottom-up tasks, the
+    # 8-words-per-lane compaction, the >= 2^30-arc hub split), forced through
+    # the PBFS_FORCE_MODES test hook so they are parity-checked here too.
+    monkeypatch.setenv("PBFS_FORCE_MODES", str(force))
+    graphs = [pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 7,
+                                           drop_self_loops=True)),
+              pb.generate(pb.GeneratorSpec(pb.GeneratorKind.UniformRandom, 14, 8, 2,
+                                           drop_self_loops=True)),
+              random_graph(3000, 9000, 11)]
+    for g in graphs:
+        dg = g.device(0, 8)
+        for s in [int(x) for x in pb.pick_sources(g, 3, 5)]:
+            want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+            for v in (V.Hybrid, V.HybridBeamer, V.NonAtomic, V.Conventional):
+                r = dg.bfs(s, pb.KernelConfig(variant=v))
+                assert np.array_equal(r.distances, want), (force, v, s)
+            r = dg.bfs(s, pb.KernelConfig(variant=V.Hybrid, hybrid_threshold_fraction=0.001))
+            assert np.array_equal(r.distances, want)
+        g.release_device()
+
+
 def test_time_run_checks_every_run(port):
     # timing.cpp:33-69 and test_instrumentation.cpp:168-198 (fault injection)
     g = make_circulant(64, [3])
