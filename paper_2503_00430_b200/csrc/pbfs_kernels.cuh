@@ -659,10 +659,11 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
 //     lane refill: a lane whose vertex is settled (parent found or list
 //     exhausted) takes the next miss, so the warp is not held to its longest
 //     scan (ER levels scan ~12 edges per vertex with a long geometric tail).
-template <typename OffT>
-__device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
-                         uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
-                         unsigned int* cursor, bool sparse) {
+template <int GPT, typename OffT>
+__device__ void bu_phase_t(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
+                           uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
+                           unsigned int* cursor) {
+  constexpr bool sparse = GPT > 1;
   constexpr int KB = kBuSlots;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -670,7 +671,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
   const unsigned warps_total = gridDim.x * kWarps;
   const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
   const uint32_t groups = (p.words + 31) / 32;
-  const uint32_t gpt = sparse ? (uint32_t)kBuSparseGroups : 1u;
+  constexpr uint32_t gpt = GPT;
   const uint32_t tasks = (groups + gpt - 1) / gpt;
   const bool beamer = p.policy == kPolicyBeamer;
   uint32_t task = gw;
@@ -678,60 +679,69 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
     // Next task index, fetched now so the cursor round trip overlaps this one.
     uint32_t nxt = 0;
     if (lane == 0) nxt = warps_total + atomicAdd(cursor, 1u);
-    uint32_t visw[kBuSparseGroups];
+    const uint32_t wbase = task * gpt * 32;  // first bitmap word of the task
+    uint32_t visw[GPT];
 #pragma unroll
-    for (int j = 0; j < kBuSparseGroups; ++j) {
-      const uint32_t w = (task * gpt + j) * 32 + lane;
-      visw[j] = ((uint32_t)j < gpt && w < p.words) ? p.visited[w] : 0xffffffffu;
+    for (int j = 0; j < GPT; ++j) {
+      const uint32_t w = wbase + j * 32 + lane;
+      visw[j] = w < p.words ? p.visited[w] : 0xffffffffu;
     }
-    // Settled groups (no unvisited vertex; padding bits are pre-set) in
-    // bulk, the rest one by one.
-    uint32_t todo = 0;
+    // One id list for the whole task (padding bits are pre-set, so settled
+    // words contribute nothing): a sparse task with a handful of unvisited
+    // vertices over 8 groups costs one pass, not eight.
+    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < kBuSparseGroups; ++j) {
-      const uint32_t g = task * gpt + j;
-      if ((uint32_t)j < gpt && g < groups) {
-        if (__any_sync(FULL, visw[j] != 0xffffffffu)) {
-          todo |= 1u << j;
-        } else if (g * 32 + lane < p.words) {
-          next[g * 32 + lane] = 0;
-        }
-      }
+    for (int j = 0; j < GPT; ++j) c += __popc(~visw[j]);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (unsigned)o) incl += x;
     }
-    while (todo) {
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t g = task * gpt + j;
-      const uint32_t w = g * 32 + lane;
-      const bool owner = w < p.words;
-      uint32_t vis = visw[0];
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    if (total == 0 || sparse) {
+      // Sparse tasks mark discoveries straight into next / visited (global
+      // atomics; there are few), so their next words start zeroed.
 #pragma unroll
-      for (int jj = 1; jj < kBuSparseGroups; ++jj) vis = j == jj ? visw[jj] : vis;
-      const uint32_t unv = ~vis;
-      const uint32_t c = __popc(unv);
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(FULL, incl, o);
-        if (lane >= (unsigned)o) incl += x;
+      for (int j = 0; j < GPT; ++j) {
+        const uint32_t w = wbase + j * 32 + lane;
+        if (w < p.words) next[w] = 0;
       }
-      const uint32_t total = __shfl_sync(FULL, incl, 31);
       if (total == 0) {
-        if (owner) next[w] = 0;
+        task = __shfl_sync(FULL, nxt, 0);
         continue;
       }
+    } else {
       found[lane] = 0;
+    }
+    // Discovery of v: the group's shared-memory word (owner writes it back),
+    // or directly into the global bitmaps on a sparse task.
+    auto mark = [&](uint32_t v) {
+      const uint32_t bit = 1u << (v & 31);
+      if (sparse) {
+        atomicOr(&next[v >> 5], bit);
+        atomicOr(&p.visited[v >> 5], bit);
+      } else {
+        atomicOr(&found[(v >> 5) - wbase], bit);
+      }
+    };
+    {
       for (uint32_t r0 = 0; r0 < total; r0 += kListCap) {
-        // This round's slice [r0, r0 + kListCap) of the ascending id list.
+        // This round's slice [r0, r0 + kListCap) of the id list (lane-major,
+        // ascending within a lane's words).
         __syncwarp();
         {
           uint32_t pos = incl - c;
-          uint32_t bits = unv;
-          while (bits && pos < r0 + kListCap) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            if (pos >= r0) list[pos - r0] = w * 32 + b;
-            ++pos;
+#pragma unroll
+          for (int j = 0; j < GPT; ++j) {
+            uint32_t bits = ~visw[j];
+            const uint32_t w = wbase + j * 32 + lane;
+            while (bits && pos < r0 + kListCap) {
+              const int b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              if (pos >= r0) list[pos - r0] = w * 32 + b;
+              ++pos;
+            }
           }
         }
         __syncwarp();
@@ -758,7 +768,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
             if (hit) {
               // kernels.cpp:362-374: first frontier neighbour wins.
               p.dist[v[q]] = nd;
-              atomicOr(&found[(v[q] >> 5) - g * 32], 1u << (v[q] & 31));
+              mark(v[q]);
               ++t.produced;
               t.edges += 1;
               if (beamer) t.degree += (unsigned long long)(__ldg(&p.rowptr[v[q] + 1]) -
@@ -834,7 +844,7 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
               scanned += (unsigned long long)(__ffs(hm) - lo);
               t.edges += scanned;
               p.dist[v] = nd;
-              atomicOr(&found[(v >> 5) - g * 32], 1u << (v & 31));
+              mark(v);
               ++t.produced;
               if (beamer) t.degree += (unsigned long long)(end - beg0);
               active = false;
@@ -849,14 +859,26 @@ __device__ void bu_phase(const Params<OffT>& p, uint32_t depth, const uint32_t* 
           }
         }
       }
-      __syncwarp();
-      if (owner) {
-        const uint32_t f = found[lane];
-        next[w] = f;
-        if (f) p.visited[w] = vis | f;
-      }
+    }
+    __syncwarp();
+    if (!sparse && wbase + lane < p.words) {
+      const uint32_t f = found[lane];
+      next[wbase + lane] = f;
+      if (f) p.visited[wbase + lane] = visw[0] | f;
     }
     task = __shfl_sync(FULL, nxt, 0);
+  }
+}
+
+template <typename OffT>
+__device__ __forceinline__ void bu_phase(const Params<OffT>& p, uint32_t depth,
+                                         const uint32_t* front, uint32_t* next, uint32_t* list,
+                                         uint32_t* found, WarpTally& t, unsigned int* cursor,
+                                         bool sparse) {
+  if (sparse) {
+    bu_phase_t<kBuSparseGroups>(p, depth, front, next, list, found, t, cursor);
+  } else {
+    bu_phase_t<1>(p, depth, front, next, list, found, t, cursor);
   }
 }
 
