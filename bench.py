@@ -422,11 +422,12 @@ def run_single(args):
     host = [pb.parbfs.pinned_empty(n, np.uint32) for _ in range(2)]
     outs = [host[i % 2] for i in range(len(sources))]
     batch_ms = []
+    widths = []
     for _ in range(max(1, args.steps)):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dg.bfs_batch(sources, cfg, outs)
+        dg.bfs_batch(sources, cfg, outs, widths)
         batch_ms.append((time.perf_counter() - t0) * 1e3)
     t_batch = statistics.median(batch_ms) / len(sources) * 1e-3  # s per source
     e2e_value = harmonic([e_r[s] / t_batch / 1e9 for s in sources])
@@ -469,10 +470,13 @@ def run_single(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 4 * NUM_SOURCES,
-                "d2h_bytes_per_step": 4 * n * NUM_SOURCES,
+                "d2h_bytes_per_step": int(sum(widths)) * n,
                 "note": "pbfs_bfs_batch C-ABI call over the 64 sources: every distance array "
                         "copied to pinned host memory (two rotating buffers) while the next "
-                        "traversal runs; median of steps; L2 flushed before each batch",
+                        "traversal runs -- from 2^25 vertices as 1 B/vertex level codes "
+                        "widened to uint32 by host threads; median of steps; L2 flushed "
+                        "before each batch",
+                "transfer_bytes_per_vertex": sorted(set(widths)),
                 "batch_ms_per_source": round(t_batch * 1e3, 3),
                 "parity_last_source": e2e_parity,
                 "sync_per_call_value": round(e2e_sync, 3)},

@@ -43,7 +43,7 @@ class Level(ctypes.Structure):
 class RunInfo(ctypes.Structure):
     _fields_ = [("levels", c_u32), ("bottom_up_levels", c_u32), ("reached", c_u64),
                 ("same_value_violations", c_u64), ("edges_examined", c_u64),
-                ("device_ms", ctypes.c_float), ("reserved", c_u32)]
+                ("device_ms", ctypes.c_float), ("transfer_width", c_u32)]
 
 
 class GraphOptions(ctypes.Structure):

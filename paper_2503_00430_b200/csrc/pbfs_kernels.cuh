@@ -99,6 +99,7 @@ constexpr unsigned long long kSmallFrontier = PBFS_SMALL_Q;
 constexpr uint32_t kForceSparseBu = 1;     // sparse bottom-up tasks at every level
 constexpr uint32_t kForceWideCompact = 2;  // 8-words-per-lane compaction
 constexpr uint32_t kForceBigSplit = 4;     // the >= 2^30-arc hub split
+constexpr uint32_t kForcePack = 8;         // pbfs_bfs_batch's narrow transfers at any size
 constexpr uint32_t kSmallChunkLog2 = PBFS_SMALL_CHUNK_LOG2;
 constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 32;      // bitmap words per warp group (one per lane)
@@ -165,6 +166,12 @@ struct alignas(128) Ctl {
   unsigned long long edges;
 };
 
+// Bytes per vertex of the packed host transfer for a traversal of `levels`
+// levels (distances 0 .. levels-1, plus the unreached marker); 4 = no pack.
+__host__ __device__ __forceinline__ uint32_t pack_width(uint32_t levels) {
+  return levels < 0xFF ? 1u : levels < 0xFFFF ? 2u : 4u;
+}
+
 struct HeavyItem {
   unsigned long long beg;
   unsigned long long end;
@@ -195,6 +202,7 @@ struct Params {
   uint32_t chunk_log2;  // log2 of edges per heavy item
   uint32_t small_chunks;  // heavy_cap covers kSmallChunkLog2 items on small frontiers
   uint32_t force;         // kForce* test hooks (PBFS_FORCE_MODES at graph creation)
+  void* pack;             // optional: narrow copy of dist for the host transfer (see pack_width)
   uint32_t source;
   int policy;
   int validate;
@@ -1165,6 +1173,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     cur_distinct = produced;
   }
 
+  // Narrow copy of the distances for a batch's host transfer: 1 B per vertex
+  // when every level fits (0xFF = unreached), else 2 B. No barrier needed:
+  // the loop ended on one, after the last level's stores.
+  if (p.pack) {
+    const uint32_t width = pack_width(depth + 1);
+    const uint4* d4 = reinterpret_cast<const uint4*>(p.dist);
+    if (width == 1) {
+      uint4* o = reinterpret_cast<uint4*>(p.pack);
+      for (unsigned long long i = tid; i < (p.n + 15) / 16; i += nthreads) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a = __ldcs(d4 + 4 * i + q);  // dist is padded to 16 entries
+          w[q] = (a.x & 0xFF) | (a.y & 0xFF) << 8 | (a.z & 0xFF) << 16 | (a.w & 0xFF) << 24;
+        }
+        o[i] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else if (width == 2) {
+      uint2* o = reinterpret_cast<uint2*>(p.pack);
+      for (unsigned long long i = tid; i < (p.n + 3) / 4; i += nthreads) {
+        const uint4 a = __ldcs(d4 + i);
+        o[i] = make_uint2((a.x & 0xFFFF) | a.y << 16, (a.z & 0xFFFF) | a.w << 16);
+      }
+    }
+  }
   if (leader) {
     ctl->levels = depth + 1;
     ctl->bu_levels = bu_levels;

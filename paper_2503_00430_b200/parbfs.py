@@ -551,10 +551,12 @@ class DeviceGraph:
                                                  r.edges_examined, r.flush_events, r.elapsed_ns))
         return BfsResult(dist, trace)
 
-    def bfs_batch(self, sources, config: KernelConfig, outs) -> List[float]:
+    def bfs_batch(self, sources, config: KernelConfig, outs,
+                  widths: Optional[list] = None) -> List[float]:
         """pbfs_bfs_batch: traversal i+1 overlaps the host copy of distances i.
         `outs[i]` receives source i's distances (entries may repeat, e.g. two
-        rotating pinned buffers). Returns per-source device ms."""
+        rotating pinned buffers). Returns per-source device ms; `widths`, if
+        given, receives the bytes per vertex each transfer moved."""
         srcs = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
         k = int(srcs.size)
         if len(outs) != k:
@@ -567,6 +569,8 @@ class DeviceGraph:
         infos = (L.RunInfo * k)()
         _check(lib.pbfs_bfs_batch(self.h, srcs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
                                   k, ctypes.byref(c), ptrs, infos))
+        if widths is not None:
+            widths[:] = [int(infos[i].transfer_width) for i in range(k)]
         return [float(infos[i].device_ms) for i in range(k)]
 
     def bfs_async(self, source: int, config: KernelConfig, stream: int = 0) -> None:

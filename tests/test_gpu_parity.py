@@ -279,8 +279,12 @@ def test_async_api_and_device_component(port):
     assert (nr, ar) == port.component(g.row_offsets, want)
 
 
-def test_batch_api_overlapped_copies(port):
-    # pbfs_bfs_batch: distances of source i land in outs[i] while i+1 runs.
+@pytest.mark.parametrize("force", ["0", "8"], ids=["plain", "packed"])
+def test_batch_api_overlapped_copies(force, port, monkeypatch):
+    # pbfs_bfs_batch: distances of source i land in outs[i] while i+1 runs;
+    # "packed" forces the narrow 1/2 B transfers + host widening that the
+    # library uses from 2^25 vertices up.
+    monkeypatch.setenv("PBFS_FORCE_MODES", force)
     g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 3,
                                      drop_self_loops=True))
     dg = g.device(0, 8)
@@ -289,8 +293,10 @@ def test_batch_api_overlapped_copies(port):
     for v in (V.Hybrid, V.Conventional, V.NonAtomic):
         cfg = pb.KernelConfig(variant=v)
         outs = [pb.parbfs.pinned_empty(g.vertex_count, np.uint32) for _ in srcs]
-        ms = dg.bfs_batch(srcs, cfg, outs)
+        widths = []
+        ms = dg.bfs_batch(srcs, cfg, outs, widths)
         assert len(ms) == len(srcs) and all(t > 0 for t in ms)
+        assert widths == [1 if force == "8" else 4] * len(srcs)
         for s, o in zip(srcs, outs):
             assert np.array_equal(o, want[s])
         # the handle's device distances are the last source's
@@ -306,6 +312,22 @@ def test_batch_api_overlapped_copies(port):
     with pytest.raises(pb.InputError, match="out of range"):
         dg.bfs_batch([0, g.vertex_count], pb.KernelConfig(variant=V.Hybrid),
                      [np.empty(g.vertex_count, np.uint32)] * 2)
+    # transfer widths: 1 B (< 255 levels, above), 2 B (< 65535 levels) and the
+    # full 4 B copy for deeper traversals; pageable outputs work too
+    for n in (600, 70000):
+        pg = make_path(n)
+        pdg = pg.device(0, 8)
+        srcs = [0, n - 1, n // 3]
+        outs = [np.empty(n, np.uint32) for _ in srcs]
+        widths = []
+        pdg.bfs_batch(srcs, pb.KernelConfig(variant=V.Hybrid), outs, widths)
+        for s, o, w in zip(srcs, outs, widths):
+            want_s = port.bfs_serial(pg.row_offsets, pg.column_indices, s)
+            assert np.array_equal(o, want_s)
+            levels = int(want_s.max()) + 1  # a path is connected
+            if force == "8":
+                assert w == (1 if levels < 255 else 2 if levels < 65535 else 4)
+        pg.release_device()
 
 
 @pytest.mark.parametrize("force", [1, 2, 4, 7])
