@@ -257,8 +257,12 @@ pbfs_status pbfs_save_csr1(const pbfs_csr* csr, const char* path);
 pbfs_status pbfs_load_csr1(const char* path, pbfs_host_csr** out);
 
 /* ---- 1D vertex-partitioned multi-GPU BFS (new) ------------
- * One partition per rank/GPU built on the device from a resident full graph:
- * hashed relabel pi, row slice (bottom-up) + column slice (top-down). Per
+ * One partition per rank/GPU built on the device from a resident full graph.
+ * Ownership by a hashed bijection pi (rank = pi(v) / local_count, balanced
+ * arcs on RMAT); numbering by gid(v) = rank * local_count + the number of
+ * lower-numbered vertices with the same owner (order-preserving, so sorted
+ * adjacency stays sorted and dense per partition). Row slice (bottom-up) +
+ * column slice (top-down). Per
  * level: pbfs_part_step (local work, writes this rank's slice of `next`),
  * then the caller allgathers the slices of `next` in place (e.g. NCCL
  * all_gather with sendbuff = next + rank * words_local), then
@@ -278,9 +282,9 @@ typedef struct pbfs_part_options {
 
 typedef struct pbfs_part_info {
   uint64_t vertex_count;
-  uint64_t padded_count;   /* pi-id space (power of two or multiple of 512*world) */
-  uint64_t local_first;    /* first owned pi-id */
-  uint64_t local_count;    /* owned pi-ids */
+  uint64_t padded_count;   /* gid space (power of two or multiple of 512*world) */
+  uint64_t local_first;    /* first owned gid */
+  uint64_t local_count;    /* owned gids */
   uint64_t local_arcs;     /* row-slice arcs (= column-slice arcs) */
   uint64_t words_total;    /* full bitmap words */
   uint64_t words_local;    /* this rank's slice: next + rank * words_local */
@@ -292,7 +296,7 @@ typedef struct pbfs_part_info {
   uint32_t reserved;
   uint32_t* frontier;      /* device, current frontier bitmap (full) */
   uint32_t* next;          /* device, next frontier bitmap (full; allgather target) */
-  uint32_t* dist_local;    /* device, local_count entries, pi-space */
+  uint32_t* dist_local;    /* device, local_count entries, gid order */
 } pbfs_part_info;
 
 /* Device pointers of a resident graph (for building partitions). */
@@ -310,16 +314,17 @@ pbfs_status pbfs_part_destroy(pbfs_part* p);
  * (owned vertices only; sum over ranks = N_r, A_r). */
 pbfs_status pbfs_part_component(pbfs_part* p, uint64_t* n_reached, uint64_t* arcs_reached);
 pbfs_status pbfs_part_get_info(const pbfs_part* p, pbfs_part_info* info);
+/* gid(v) (the id used by the bitmaps, queues and dist_local). */
 pbfs_status pbfs_part_relabel(const pbfs_part* p, uint64_t v, uint64_t* pi_v);
 pbfs_status pbfs_part_begin(pbfs_part* p, uint32_t source, const pbfs_config* cfg, void* stream);
 pbfs_status pbfs_part_step(pbfs_part* p, void* stream);
 pbfs_status pbfs_part_end_level(pbfs_part* p, void* stream, uint32_t* done, pbfs_level* rec);
 pbfs_status pbfs_part_sync(pbfs_part* p, void* stream);
-/* dist[v] = dist_pi[pi(v)] for v < vertex_count (dist_pi: padded_count entries,
- * the ranks' dist_local slices concatenated). */
+/* dist[v] = dist_pi[gid(v)] for v < vertex_count (dist_pi: padded_count
+ * entries, the ranks' dist_local slices concatenated). */
 pbfs_status pbfs_part_unrelabel(pbfs_part* p, const uint32_t* dist_pi, uint32_t* dist, void* stream);
 /* Host-side helpers: copy this rank's dist_local (local_count u32) to host;
- * un-relabel a host pi-space array (padded_count entries) into dist (n). */
+ * un-relabel a host gid-order array (padded_count entries) into dist (n). */
 pbfs_status pbfs_part_copy_dist(pbfs_part* p, uint32_t* host_out);
 pbfs_status pbfs_part_unrelabel_host(const pbfs_part* p, const uint32_t* dist_pi, uint32_t* dist);
 

@@ -1,15 +1,21 @@
 // 1D vertex-partitioned BFS: one partition per GPU, one
 // frontier-bitmap allgather per level.
 //
-//   * Vertices are relabelled by a bijective hash pi on [0, 2^k) (multiply by
-//     an odd constant, xor-shift, multiply again; identity + padding when n is
-//     not a power of two) so every rank owns an equal share of the RMAT arcs
+//   * Ownership by a bijective hash pi on [0, 2^k) (multiply by an odd
+//     constant, xor-shift, multiply again; identity + padding when n is not a
+//     power of two): rank r owns the vertices with pi(v) in [r*nloc,
+//     (r+1)*nloc), so every rank holds an equal share of the RMAT arcs
 //     (unpermuted RMAT puts ~42 % of arcs on one of 8 contiguous ranks).
-//   * Rank r owns pi-ids [r*nloc, (r+1)*nloc) and stores
+//   * Numbering by gid(v) = owner * nloc + the vertex's rank among its
+//     owner's vertices in original order: order-preserving inside each
+//     partition, so sorted adjacency lists stay sorted (and RMAT's dense
+//     low-id hub region stays dense) -- the probe locality the single-GPU
+//     kernel lives on (pi's own order costs ~40 % of top-down speed).
+//   * Rank r owns gids [r*nloc, (r+1)*nloc) and stores
 //       - the ROW slice: full adjacency of its owned vertices (neighbours as
-//         global pi-ids) -- bottom-up scans it against the replicated frontier;
-//       - the COLUMN slice: for every global pi-id u, u's owned neighbours as
-//         local ids (the transpose of the row slice; the graph is symmetric)
+//         gids) -- bottom-up scans it against the replicated frontier;
+//       - the COLUMN slice: for every gid u, u's owned neighbours as local ids,
+//         ascending (u's own list filtered by owner; the graph is symmetric)
 //         -- top-down expands the whole replicated frontier over it.
 //     Either way discoveries are owner-local: dist / visited stores stay
 //     local and the claim atomics never cross a GPU.
@@ -88,49 +94,106 @@ __host__ __device__ __forceinline__ uint64_t pi_inv(const Relabel& r, uint64_t y
 }
 
 // ---- partition-build kernels ---------------------------------------------------
-template <typename OffT>
-__global__ void k_local_degrees(const OffT* __restrict__ rowptr, uint64_t n, Relabel rl,
-                                uint64_t lo, uint64_t nloc, unsigned long long* deg) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t v = pi_inv(rl, lo + i);
-    deg[i] = v < n ? (unsigned long long)(rowptr[v + 1] - rowptr[v]) : 0ull;
+// Ownership: rank of v = pi(v) / nloc (the hash balances RMAT's arcs).
+// Numbering: gid(v) = owner * nloc + (number of vertices u < v with the same
+// owner) -- the ORDER-PRESERVING local index. A hub's sorted neighbour list
+// stays sorted (and, on RMAT, dense in low ids) inside every partition, so
+// the probes of a warp hit few bitmap lines, as on one GPU; pi's own order
+// would scatter them.
+__global__ void k_owner_flags(uint64_t n, Relabel rl, uint64_t nloc, uint32_t r,
+                              uint32_t* flags) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    flags[v] = pi_fwd(rl, v) / nloc == r ? 1u : 0u;
   }
 }
 
-// Warp per owned vertex: relabelled neighbour list into the row slice, and
-// a count of each neighbour for the column slice.
-template <typename OffT>
-__global__ void k_fill_rows(const OffT* __restrict__ rowptr, const uint32_t* __restrict__ col,
-                            uint64_t n, Relabel rl, uint64_t lo, uint64_t nloc,
-                            const unsigned long long* __restrict__ rowloc, uint32_t* colrow,
-                            unsigned long long* colcnt) {
-  const unsigned lane = threadIdx.x & 31;
-  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; i < nloc;
-       i += warps) {
-    const uint64_t v = pi_inv(rl, lo + i);
-    if (v >= n) continue;
-    const uint64_t b = rowptr[v], e = rowptr[v + 1], out = rowloc[i];
-    for (uint64_t k = b + lane; k < e; k += 32) {
-      const uint32_t u = (uint32_t)pi_fwd(rl, col[k]);
-      colrow[out + (k - b)] = u;
-      atomicAdd(&colcnt[u], 1ull);
+__global__ void k_owner_gid(uint64_t n, Relabel rl, uint64_t nloc, uint32_t r,
+                            const uint32_t* __restrict__ rank_in, uint32_t* gid, uint32_t* inv) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    if (pi_fwd(rl, v) / nloc == r) {
+      const uint64_t g = r * nloc + rank_in[v];
+      gid[v] = (uint32_t)g;
+      inv[g] = (uint32_t)v;
     }
   }
 }
 
-__global__ void k_fill_cols(const unsigned long long* __restrict__ rowloc,
-                            const uint32_t* __restrict__ colrow, uint64_t nloc,
-                            unsigned long long* cursor, uint32_t* colcol) {
+template <typename OffT>
+__global__ void k_local_degrees(const OffT* __restrict__ rowptr, uint64_t n,
+                                const uint32_t* __restrict__ inv, uint64_t lo, uint64_t nloc,
+                                unsigned long long* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = inv[lo + i];
+    deg[i] = v < n ? (unsigned long long)(rowptr[v + 1] - rowptr[v]) : 0ull;
+  }
+}
+
+// Warp per owned vertex: its neighbour list, renumbered to gids, is its row
+// of the row slice (bottom-up).
+template <typename OffT>
+__global__ void k_fill_rows(const OffT* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                            uint64_t n, const uint32_t* __restrict__ gid,
+                            const uint32_t* __restrict__ inv, uint64_t lo, uint64_t nloc,
+                            const unsigned long long* __restrict__ rowloc, uint32_t* colrow) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
   for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; i < nloc;
        i += warps) {
-    for (uint64_t k = rowloc[i] + lane; k < rowloc[i + 1]; k += 32) {
-      const uint32_t u = colrow[k];
-      const unsigned long long pos = atomicAdd(&cursor[u], 1ull);
-      colcol[pos] = (uint32_t)i;
+    const uint64_t v = inv[lo + i];
+    if (v >= n) continue;
+    const uint64_t b = rowptr[v], e = rowptr[v + 1], out = rowloc[i];
+    for (uint64_t k = b + lane; k < e; k += 32) colrow[out + (k - b)] = gid[col[k]];
+  }
+}
+
+// Column slice (top-down): for every vertex u, its neighbours owned by this
+// rank as local ids. The graph is symmetric, so that is u's own neighbour
+// list filtered by owner -- written in list order, hence ascending. Pass 1
+// counts (indexed by gid(u)), pass 2 fills with a warp ballot compaction.
+template <typename OffT>
+__global__ void k_col_count(const OffT* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                            uint64_t n, const uint32_t* __restrict__ gid, uint64_t lo,
+                            uint64_t nloc, unsigned long long* colcnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t u = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; u < n;
+       u += warps) {
+    unsigned long long c = 0;
+    for (uint64_t k = rowptr[u] + lane; k < rowptr[u + 1]; k += 32) {
+      const uint64_t w = gid[col[k]];
+      c += (w >= lo && w < lo + nloc) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) colcnt[gid[u]] = c;
+  }
+}
+
+template <typename OffT>
+__global__ void k_col_fill(const OffT* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                           uint64_t n, const uint32_t* __restrict__ gid, uint64_t lo,
+                           uint64_t nloc, const unsigned long long* __restrict__ colptr,
+                           uint32_t* colcol) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t u = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; u < n;
+       u += warps) {
+    unsigned long long out = colptr[gid[u]];
+    const uint64_t e = rowptr[u + 1];
+    for (uint64_t k0 = rowptr[u]; k0 < e; k0 += 32) {
+      const uint64_t k = k0 + lane;
+      uint64_t w = 0;
+      bool mine = false;
+      if (k < e) {
+        w = gid[col[k]];
+        mine = w >= lo && w < lo + nloc;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) colcol[out + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)(w - lo);
+      out += __popc(bal);
     }
   }
 }
@@ -265,11 +328,11 @@ __global__ void k_set_qlen(const LevelCnt* cnt, PartState* st) {
   st->qlen = cnt->conv_count;
 }
 
-__global__ void k_unrelabel(const uint32_t* __restrict__ dist_pi, uint64_t n, Relabel rl,
-                            uint32_t* dist) {
+__global__ void k_unrelabel(const uint32_t* __restrict__ dist_pi, uint64_t n,
+                            const uint32_t* __restrict__ gid, uint32_t* dist) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    dist[v] = dist_pi[pi_fwd(rl, v)];
+    dist[v] = dist_pi[gid[v]];
   }
 }
 
@@ -290,10 +353,15 @@ struct pbfs_part {
   unsigned long long* rowloc = nullptr;  // nloc + 1
   uint32_t* colrow = nullptr;            // m_loc, global pi-ids
   uint32_t* first = nullptr;             // nloc + 1: first row-slice neighbour
+  // order-preserving numbering (k_owner_gid): vertex -> gid, gid -> vertex
+  uint32_t* gid = nullptr;               // n
+  uint32_t* inv = nullptr;               // npad (0xFFFFFFFF = padding)
+  std::vector<uint32_t> gid_host;        // lazily copied for pbfs_part_unrelabel_host
   // column slice (top-down)
   unsigned long long* colptr = nullptr;  // npad + 1
   uint32_t* colcol = nullptr;            // m_loc, local ids
   uint64_t col_maxdeg = 0, heavy_cap = 0;
+  size_t persist = 0;  // persisting-L2 set-aside available to the level kernels
   // traversal state
   uint32_t* dist = nullptr;      // nloc
   uint32_t* visited = nullptr;   // lwords
@@ -350,6 +418,33 @@ void part_release(pbfs_part* g) {
   delete g;
 }
 
+// Launch on `s` with a persisting-L2 window over [base, base + bytes): the
+// top-down kernels keep the local visited slice resident against the col
+// stream, bottom-up the frontier bitmap it probes.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_window(void (*kern)(KArgs...), int grid, cudaStream_t s, const void* base,
+                          size_t bytes, size_t persist, Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kThreads);
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  int nattr = 0;
+  if (persist && bytes) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr[0].val.accessPolicyWindow.num_bytes = bytes;
+    attr[0].val.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(persist) / static_cast<float>(bytes));
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nattr = 1;
+  }
+  lc.attrs = attr;
+  lc.numAttrs = nattr;
+  return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
+
 Params<unsigned long long> td_params(const pbfs_part* g) {
   Params<unsigned long long> p{};
   p.rowptr = g->colptr;
@@ -388,44 +483,75 @@ template <typename OffT>
 pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* col) {
   cudaStream_t s = g->stream;
   const int blocks = g->grid;
-  unsigned long long* deg = nullptr;
   pbfs_status st;
-  if ((st = palloc(g, &g->rowloc, (g->nloc + 1) * 8)) != PBFS_OK) return st;
-  if ((st = palloc(g, &deg, (g->nloc + 1) * 8)) != PBFS_OK) return st;
-  PCUDA(cudaMemsetAsync(deg, 0, (g->nloc + 1) * 8, s), "memset");
-  k_local_degrees<OffT><<<blocks, 256, 0, s>>>(rowptr, g->n, g->rl, g->lo, g->nloc, deg);
-  // rowloc = exclusive scan of deg (nloc + 1 entries; deg[nloc] = 0)
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg, g->rowloc, (int64_t)(g->nloc + 1), s);
-  size_t tmp2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, deg, g->rowloc, (int64_t)(g->npad + 1), s);
-  tmp_bytes = std::max(tmp_bytes, tmp2);
+  // Scan scratch sized for every scan below.
+  size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, static_cast<uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), (int64_t)g->n, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, static_cast<unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), (int64_t)(g->nloc + 1), s);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, static_cast<unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), (int64_t)(g->npad + 1), s);
+  tmp_bytes = std::max({t1, t2, t3, size_t{16}});
   void* tmp = nullptr;
   PCUDA(cudaMalloc(&tmp, tmp_bytes), "scan scratch");
+  auto bail = [&](pbfs_status x) {
+    cudaFree(tmp);
+    return x;
+  };
+  // 1. gid / inv maps: one flag scan per owner rank.
+  if ((st = palloc(g, &g->gid, g->n * 4 + 16)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->inv, g->npad * 4 + 16)) != PBFS_OK) return bail(st);
+  PCUDA(cudaMemsetAsync(g->inv, 0xFF, g->npad * 4, s), "memset");
+  {
+    uint32_t *flags = nullptr, *rank_in = nullptr;
+    PCUDA(cudaMalloc(&flags, g->n * 4 + 16), "flags");
+    if (cudaMalloc(&rank_in, g->n * 4 + 16) != cudaSuccess) {
+      cudaFree(flags);
+      cudaGetLastError();
+      return bail(fail(PBFS_E_CAPACITY, "partition build scratch"));
+    }
+    for (uint32_t r = 0; r < g->world; ++r) {
+      k_owner_flags<<<blocks, 256, 0, s>>>(g->n, g->rl, g->nloc, r, flags);
+      cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, rank_in, (int64_t)g->n, s);
+      k_owner_gid<<<blocks, 256, 0, s>>>(g->n, g->rl, g->nloc, r, rank_in, g->gid, g->inv);
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(flags);
+    cudaFree(rank_in);
+    if (e != cudaSuccess) return bail(cuda_fail_p(e, "gid maps"));
+  }
+  // 2. Row slice: owned vertices' lists, neighbours as gids.
+  unsigned long long* deg = nullptr;
+  if ((st = palloc(g, &g->rowloc, (g->nloc + 1) * 8)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &deg, (g->nloc + 1) * 8)) != PBFS_OK) return bail(st);
+  PCUDA(cudaMemsetAsync(deg, 0, (g->nloc + 1) * 8, s), "memset");
+  k_local_degrees<OffT><<<blocks, 256, 0, s>>>(rowptr, g->n, g->inv, g->lo, g->nloc, deg);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, g->rowloc, (int64_t)(g->nloc + 1), s);
   unsigned long long mloc = 0;
   PCUDA(cudaMemcpyAsync(&mloc, g->rowloc + g->nloc, 8, cudaMemcpyDeviceToHost, s), "read m_loc");
   PCUDA(cudaStreamSynchronize(s), "partition scan");
   g->m_loc = mloc;
+  if ((st = palloc(g, &g->colrow, (g->m_loc + 16) * 4)) != PBFS_OK) return bail(st);
+  k_fill_rows<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->gid, g->inv, g->lo, g->nloc,
+                                           g->rowloc, g->colrow);
+  // 3. Column slice: every vertex's owned neighbours, ascending local ids.
   unsigned long long* colcnt = nullptr;
-  if ((st = palloc(g, &g->colrow, (g->m_loc + 16) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
-  if ((st = palloc(g, &colcnt, (g->npad + 1) * 8)) != PBFS_OK) { cudaFree(tmp); return st; }
+  if ((st = palloc(g, &colcnt, (g->npad + 1) * 8)) != PBFS_OK) return bail(st);
   PCUDA(cudaMemsetAsync(colcnt, 0, (g->npad + 1) * 8, s), "memset");
-  k_fill_rows<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->rl, g->lo, g->nloc, g->rowloc,
-                                           g->colrow, colcnt);
-  if ((st = palloc(g, &g->colptr, (g->npad + 1) * 8)) != PBFS_OK) { cudaFree(tmp); return st; }
+  k_col_count<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->gid, g->lo, g->nloc, colcnt);
+  if ((st = palloc(g, &g->colptr, (g->npad + 1) * 8)) != PBFS_OK) return bail(st);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, colcnt, g->colptr, (int64_t)(g->npad + 1), s);
-  if ((st = palloc(g, &g->colcol, (g->m_loc + 8) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
-  // cursor = colptr copy (reuse colcnt)
-  PCUDA(cudaMemcpyAsync(colcnt, g->colptr, (g->npad + 1) * 8, cudaMemcpyDeviceToDevice, s), "copy");
-  k_fill_cols<<<blocks, 256, 0, s>>>(g->rowloc, g->colrow, g->nloc, colcnt, g->colcol);
+  if ((st = palloc(g, &g->colcol, (g->m_loc + 8) * 4)) != PBFS_OK) return bail(st);
+  k_col_fill<OffT><<<blocks, 256, 0, s>>>(rowptr, col, g->n, g->gid, g->lo, g->nloc, g->colptr,
+                                          g->colcol);
   unsigned long long* stats = deg;  // reuse: [0] maxdeg, [1] heavy items
   PCUDA(cudaMemsetAsync(stats, 0, 16, s), "memset");
   k_col_stats<<<blocks, 256, 0, s>>>(g->colptr, g->npad, stats, stats + 1);
   unsigned long long hs[2];
   PCUDA(cudaMemcpyAsync(hs, stats, 16, cudaMemcpyDeviceToHost, s), "read stats");
-  if ((st = palloc(g, &g->mask, g->lwords * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
-  if ((st = palloc(g, &g->first, (g->nloc + 1) * 4)) != PBFS_OK) { cudaFree(tmp); return st; }
+  if ((st = palloc(g, &g->mask, g->lwords * 4)) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->first, (g->nloc + 1) * 4)) != PBFS_OK) return bail(st);
   k_first_nbr<<<blocks, 256, 0, s>>>(g->rowloc, g->colrow, g->nloc, g->first);
   k_local_mask<<<blocks, 256, 0, s>>>(g->rowloc, g->nloc, g->lwords, g->mask);
   PCUDA(cudaGetLastError(), "partition kernels");
@@ -549,6 +675,19 @@ pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void*
   if ((e = cudaMallocHost(&g->st_host, sizeof(PartState))) != cudaSuccess)
     return bail(cuda_fail_p(e, "pinned state"));
   PCUDA(cudaMemset(g->ctl, 0, sizeof(Ctl)), "memset");
+  // Persisting-L2 set-aside (process-wide limit, only ever raised) for the
+  // level kernels' windows: the larger of the local visited slice and the
+  // full frontier bitmap.
+  if (prop.persistingL2CacheMaxSize > 0) {
+    const size_t want = std::min<size_t>(std::max<size_t>(g->lwords, g->words_total) * 4,
+                                         prop.persistingL2CacheMaxSize);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur >= want || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+      g->persist = std::max(cur, want);
+    }
+    cudaGetLastError();
+  }
   *out = g;
   return PBFS_OK;
 }
@@ -585,7 +724,10 @@ pbfs_status pbfs_part_get_info(const pbfs_part* g, pbfs_part_info* info) {
 pbfs_status pbfs_part_relabel(const pbfs_part* g, uint64_t v, uint64_t* pi_v) {
   if (!g || !pi_v) return fail(PBFS_E_INPUT, "null argument");
   if (v >= g->n) return fail(PBFS_E_INPUT, "vertex out of range");
-  *pi_v = pi_fwd(g->rl, v);
+  uint32_t x = 0;
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PCUDA(cudaMemcpy(&x, g->gid + v, 4, cudaMemcpyDeviceToHost), "gid");
+  *pi_v = x;
   return PBFS_OK;
 }
 
@@ -608,7 +750,9 @@ pbfs_status pbfs_part_begin(pbfs_part* g, uint32_t source, const pbfs_config* cf
   g->fcur = 0;
   g->qcur = 0;
   g->depth = 0;
-  const uint64_t spi = pi_fwd(g->rl, source);
+  uint32_t spi32 = 0;
+  PCUDA(cudaMemcpy(&spi32, g->gid + source, 4, cudaMemcpyDeviceToHost), "source gid");
+  const uint64_t spi = spi32;
   const uint64_t clear_lo = g->shared ? g->lo / 32 : 0;
   const uint64_t clear_words = g->shared ? g->lwords : g->words_total;
   const bool set_bit = !g->shared || (spi >= g->lo && spi < g->lo + g->nloc);
@@ -635,15 +779,20 @@ pbfs_status pbfs_part_step(pbfs_part* g, void* stream) {
     // Own slice of the next bitmap must be zero before claims mark it.
     k_clear<<<g->grid, 256, 0, s>>>(next_local, g->lwords);
     Params<unsigned long long> p = td_params(g);
-    k_td_light<unsigned long long><<<g->grid, kThreads, 0, s>>>(
-        p, g->depth, g->queue[g->qcur], g->st, g->queue[g->qcur ^ 1], next_local);
+    const size_t vbytes = g->lwords * 4;
+    PCUDA(launch_window(k_td_light<unsigned long long>, g->grid, s, g->visited, vbytes, g->persist,
+                        p, g->depth, g->queue[g->qcur], g->st, g->queue[g->qcur ^ 1], next_local),
+          "top-down launch");
     if (g->col_maxdeg > kHeavyDeg) {
-      k_td_heavy<unsigned long long><<<g->grid, kThreads, 0, s>>>(p, g->depth,
-                                                                 g->queue[g->qcur ^ 1], next_local);
+      PCUDA(launch_window(k_td_heavy<unsigned long long>, g->grid, s, g->visited, vbytes,
+                          g->persist, p, g->depth, g->queue[g->qcur ^ 1], next_local),
+            "top-down launch");
     }
   } else {
     Params<unsigned long long> p = bu_params(g);
-    k_bu<unsigned long long><<<g->grid, kThreads, 0, s>>>(p, g->depth, g->bm[g->fcur], next_local);
+    PCUDA(launch_window(k_bu<unsigned long long>, g->grid, s, g->bm[g->fcur], g->words_total * 4,
+                        g->persist, p, g->depth, g->bm[g->fcur], next_local),
+          "bottom-up launch");
   }
   PCUDA(cudaGetLastError(), "level launch");
   return PBFS_OK;
@@ -703,7 +852,7 @@ pbfs_status pbfs_part_unrelabel(pbfs_part* g, const uint32_t* dist_pi, uint32_t*
   if (!g || !dist_pi || !dist) return fail(PBFS_E_INPUT, "null argument");
   PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
-  k_unrelabel<<<g->grid, 256, 0, s>>>(dist_pi, g->n, g->rl, dist);
+  k_unrelabel<<<g->grid, 256, 0, s>>>(dist_pi, g->n, g->gid, dist);
   PCUDA(cudaGetLastError(), "unrelabel");
   return PBFS_OK;
 }
@@ -734,7 +883,13 @@ pbfs_status pbfs_part_copy_dist(pbfs_part* g, uint32_t* host_out) {
 
 pbfs_status pbfs_part_unrelabel_host(const pbfs_part* g, const uint32_t* dist_pi, uint32_t* dist) {
   if (!g || !dist_pi || !dist) return fail(PBFS_E_INPUT, "null argument");
-  for (uint64_t v = 0; v < g->n; ++v) dist[v] = dist_pi[pi_fwd(g->rl, v)];
+  auto* gm = const_cast<pbfs_part*>(g);
+  if (gm->gid_host.size() != g->n) {
+    gm->gid_host.resize(g->n);
+    PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+    PCUDA(cudaMemcpy(gm->gid_host.data(), g->gid, g->n * 4, cudaMemcpyDeviceToHost), "gid map");
+  }
+  for (uint64_t v = 0; v < g->n; ++v) dist[v] = dist_pi[gm->gid_host[v]];
   return PBFS_OK;
 }
 

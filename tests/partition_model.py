@@ -1,6 +1,7 @@
 """TEST MODEL of the 1D vertex-partition protocol (csrc/pbfs_part.cu), in numpy:
-same relabel pi, same row/column slices, same per-level allgather of the
-next-frontier bitmap slices. Used by the gloo world-size-2 CPU tests to
+same ownership (hashed pi) and order-preserving gid numbering, same
+row/column slices, same per-level allgather of the next-frontier bitmap
+slices. Used by the gloo world-size-2 CPU tests to
 check the host-side partition logic and the exchange protocol without a GPU.
 """
 import numpy as np
@@ -41,11 +42,23 @@ class Relabel:
         return (x * np.uint64(self.b)) & m
 
 
-def build_partition(offsets, col, n, rank, world, hashed=True):
+def gid_map(n, world, hashed=True):
+    """gid(v) = owner * nloc + rank of v among its owner's vertices (original
+    order), owner = pi(v) // nloc."""
     rl = Relabel(n, world, hashed)
     nloc = rl.npad // world
+    owner = rl.fwd(np.arange(n, dtype=np.uint64)).astype(np.int64) // nloc
+    order = np.argsort(owner, kind="stable")
+    counts = np.bincount(owner, minlength=world)
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    gid = np.empty(n, dtype=np.int64)
+    gid[order] = owner[order] * nloc + (np.arange(n) - starts[owner[order]])
+    return rl, nloc, gid
+
+
+def build_partition(offsets, col, n, rank, world, hashed=True):
+    rl, nloc, pi = gid_map(n, world, hashed)
     lo = rank * nloc
-    pi = rl.fwd(np.arange(n, dtype=np.uint64)).astype(np.int64)
     inv = np.full(rl.npad, -1, dtype=np.int64)
     inv[pi] = np.arange(n)
     rows = []

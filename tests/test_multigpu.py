@@ -130,14 +130,26 @@ def test_loopback_identity_relabel_and_padding(port):
     assert np.array_equal(got, port.bfs_serial(g.row_offsets, g.column_indices, 17))
 
 
+def test_gid_map_is_order_preserving_and_balanced():
+    for n, world in [(1 << 14, 2), (1 << 16, 8), (5000, 4)]:
+        rl, nloc, gid = pm.gid_map(n, world)
+        assert len(np.unique(gid)) == n and int(gid.max()) < rl.npad
+        owner = gid // nloc
+        for r in range(world):
+            mine = np.nonzero(owner == r)[0]          # ascending vertex ids
+            assert (np.diff(gid[mine]) == 1).all()   # consecutive, same order
+        if rl.hashed:
+            assert (np.bincount(owner, minlength=world) == nloc).all()
+
+
 @pytest.mark.gpu
 def test_device_relabel_matches_model():
     import ctypes
     import paper_2503_00430_b200 as pb
     g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 14, 4, 2))
     p = pb.PartitionedGraph(g.device(0, 8), 1, 4)
-    rl = pm.Relabel(g.vertex_count, 4)
+    _, _, gid = pm.gid_map(g.vertex_count, 4)
     out = ctypes.c_uint64()
     for v in [0, 1, 2, 777, g.vertex_count - 1]:
         pb.parbfs._check(pb.parbfs.lib.pbfs_part_relabel(p.h, v, ctypes.byref(out)))
-        assert out.value == int(rl.fwd(v))
+        assert out.value == int(gid[v])
