@@ -569,6 +569,7 @@ def run_partitioned(args):
         f"{[p.info()['local_arcs'] for p in parts]}")
 
     launches = [0]
+    LOOKAHEAD = int(os.environ.get("PBFS_PART_LOOKAHEAD", "4"))
 
     def exchange():
         if multi:
@@ -580,16 +581,21 @@ def run_partitioned(args):
                 coll(tdist.all_gather_into_tensor, full, full[rank * wl:(rank + 1) * wl].clone())
 
     def bfs(s):
+        # Levels are enqueued LOOKAHEAD at a time (direction, termination and
+        # queues are decided on the device; levels past the end are no-ops),
+        # then one poll: a host sync every few levels instead of every level.
         for p in parts:
             p.begin(s, cfg, sptr)
         while True:
-            for p in parts:
-                p.step(sptr)
-                launches[0] += 3
-            exchange()
-            res = [p.end_level(sptr) for p in parts]
-            launches[0] += 2 * len(parts)
-            if res[0][0]:
+            for _ in range(LOOKAHEAD):
+                for p in parts:
+                    p.step(sptr)
+                    launches[0] += 4
+                exchange()
+                for p in parts:
+                    p.end_level_async(sptr)
+                    launches[0] += 4
+            if parts[0].poll(sptr)[0]:
                 return
 
     def reduce_sum(vals):

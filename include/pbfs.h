@@ -317,7 +317,19 @@ pbfs_status pbfs_part_get_info(const pbfs_part* p, pbfs_part_info* info);
 /* gid(v) (the id used by the bitmaps, queues and dist_local). */
 pbfs_status pbfs_part_relabel(const pbfs_part* p, uint64_t v, uint64_t* pi_v);
 pbfs_status pbfs_part_begin(pbfs_part* p, uint32_t source, const pbfs_config* cfg, void* stream);
+/* One level = pbfs_part_step, the caller's allgather of info.next, then
+ * pbfs_part_end_level_async. The level's direction, termination and queue
+ * live on the device, so a caller may enqueue several levels ahead and
+ * pbfs_part_poll (which synchronises) only now and then: levels enqueued past
+ * the end are no-ops. info.next is the allgather target of the NEXT level to
+ * be stepped (it alternates every level). */
 pbfs_status pbfs_part_step(pbfs_part* p, void* stream);
+pbfs_status pbfs_part_end_level_async(pbfs_part* p, void* stream);
+/* done: the traversal has finished; levels: levels recorded so far. */
+pbfs_status pbfs_part_poll(pbfs_part* p, void* stream, uint32_t* done, uint32_t* levels);
+/* The device record of level `depth` (this rank's edges_examined). */
+pbfs_status pbfs_part_level_record(pbfs_part* p, uint32_t depth, pbfs_level* rec);
+/* end_level_async + poll + the level's record (one sync per level). */
 pbfs_status pbfs_part_end_level(pbfs_part* p, void* stream, uint32_t* done, pbfs_level* rec);
 pbfs_status pbfs_part_sync(pbfs_part* p, void* stream);
 /* dist[v] = dist_pi[gid(v)] for v < vertex_count (dist_pi: padded_count

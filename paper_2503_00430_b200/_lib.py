@@ -120,6 +120,9 @@ SIGNATURES = [
     ("pbfs_part_begin", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),
     ("pbfs_part_step", ctypes.c_int, [c_vp, c_vp]),
     ("pbfs_part_end_level", ctypes.c_int, [c_vp, c_vp, P(c_u32), P(Level)]),
+    ("pbfs_part_end_level_async", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_part_poll", ctypes.c_int, [c_vp, c_vp, P(c_u32), P(c_u32)]),
+    ("pbfs_part_level_record", ctypes.c_int, [c_vp, c_u32, P(Level)]),
     ("pbfs_part_sync", ctypes.c_int, [c_vp, c_vp]),
     ("pbfs_part_unrelabel", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("pbfs_part_copy_dist", ctypes.c_int, [c_vp, c_vp]),

@@ -233,18 +233,31 @@ __global__ void k_local_mask(const unsigned long long* __restrict__ rowloc, uint
 }
 
 // ---- per-level kernels -------------------------------------------------------------
+// The level state lives on the device so a host can enqueue several levels
+// ahead without a sync: every level kernel reads it first and returns when
+// the traversal is done or the level goes the other direction, and
+// k_decide (one thread) applies the 5 % rule. The host's only per-level
+// knowledge is the bitmap parity (fcur flips every level), which names the
+// `next` buffer it allgathers.
+constexpr uint32_t kPartRecCap = 1u << 16;  // device level records kept per traversal
+
 struct PartState {
-  unsigned long long qlen;
-  unsigned long long distinct;
+  unsigned long long qlen;          // current top-down queue length
+  unsigned long long distinct;      // popcount of the gathered next bitmap
+  unsigned long long cur_distinct;  // current frontier size
+  unsigned int td, fcur, depth, done, compact;
+  unsigned int pad[3];
 };
 
 __global__ void k_begin(uint32_t* dist, uint32_t* visited, const uint32_t* mask, uint64_t nloc,
                         uint64_t lwords, uint32_t* front, uint32_t* next, uint64_t clear_lo,
-                        uint64_t clear_words, uint64_t src_pi, uint64_t lo, bool set_src_bit,
-                        uint32_t* queue, PartState* st) {
+                        uint64_t clear_words, const uint32_t* __restrict__ gid, uint32_t source,
+                        uint64_t lo, bool shared, uint32_t* queue, PartState* st, bool seed_td) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t src_pi = gid[source];
   const bool owner = src_pi >= lo && src_pi < lo + nloc;
+  const bool set_src_bit = !shared || owner;
   for (uint64_t i = tid; i < nloc; i += nth) dist[i] = (owner && i == src_pi - lo) ? 0u : kUnreached;
   for (uint64_t w = tid; w < lwords; w += nth) {
     uint32_t m = mask[w];
@@ -258,12 +271,19 @@ __global__ void k_begin(uint32_t* dist, uint32_t* visited, const uint32_t* mask,
   }
   if (tid == 0) {
     queue[0] = (uint32_t)src_pi;
-    st->qlen = 1;
-    st->distinct = 1;
+    PartState z{};
+    z.qlen = 1;
+    z.cur_distinct = 1;
+    z.td = seed_td ? 1u : 0u;
+    *st = z;
   }
 }
 
-__global__ void k_clear(uint32_t* p, uint64_t words) {
+// Zero this rank's slice of the next bitmap (top-down marks into it).
+__global__ void k_clear(uint32_t* bm0, uint32_t* bm1, uint64_t lo_word, uint64_t words,
+                        const PartState* st) {
+  if (st->done || !st->td) return;
+  uint32_t* p = (st->fcur ? bm0 : bm1) + lo_word;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
        w += (uint64_t)gridDim.x * blockDim.x) {
     p[w] = 0u;
@@ -271,44 +291,56 @@ __global__ void k_clear(uint32_t* p, uint64_t words) {
 }
 
 template <typename OffT>
-__global__ void __launch_bounds__(kThreads) k_td_light(Params<OffT> p, uint32_t depth,
-                                                       const uint32_t* qin, const PartState* st,
-                                                       uint32_t* qout, uint32_t* mark) {
+__global__ void __launch_bounds__(kThreads) k_td_light(Params<OffT> p, uint32_t* q0,
+                                                       uint32_t* q1, uint32_t* bm0, uint32_t* bm1,
+                                                       uint64_t lo_word, const PartState* st) {
+  if (st->done || !st->td) return;
   __shared__ uint32_t s_buf[kWarps][kPushBuf];
   WarpPush wp{s_buf[threadIdx.x >> 5], 0};
   WarpTally t;
   LevelCnt* cnt = &p.ctl->cnt[0];
-  td_phase_light<kClaimBitmap>(p, depth, qin, st->qlen, qout, wp, cnt, t, mark, nullptr);
-  wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  uint32_t* mark = (st->fcur ? bm0 : bm1) + lo_word;
+  td_phase_light<kClaimBitmap>(p, st->depth, q0, st->qlen, q1, wp, cnt, t, mark, nullptr);
+  wp.flush(q1, &cnt->raw, p.qcap, &p.ctl->overflow);
   warp_flush_tally(cnt, t, false);
 }
 
 template <typename OffT>
-__global__ void __launch_bounds__(kThreads) k_td_heavy(Params<OffT> p, uint32_t depth,
-                                                       uint32_t* qout, uint32_t* mark) {
+__global__ void __launch_bounds__(kThreads) k_td_heavy(Params<OffT> p, uint32_t* q1,
+                                                       uint32_t* bm0, uint32_t* bm1,
+                                                       uint64_t lo_word, const PartState* st) {
+  if (st->done || !st->td) return;
   __shared__ uint32_t s_buf[kWarps][kPushBuf];
   WarpPush wp{s_buf[threadIdx.x >> 5], 0};
   WarpTally t;
   LevelCnt* cnt = &p.ctl->cnt[0];
+  uint32_t* mark = (st->fcur ? bm0 : bm1) + lo_word;
   const unsigned int items = *(volatile unsigned int*)&cnt->heavy_count;
-  if (items) td_phase_heavy<kClaimBitmap>(p, depth, items, qout, wp, cnt, t, mark);
-  wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  if (items) td_phase_heavy<kClaimBitmap>(p, st->depth, items, q1, wp, cnt, t, mark);
+  wp.flush(q1, &cnt->raw, p.qcap, &p.ctl->overflow);
   warp_flush_tally(cnt, t, false);
 }
 
 template <typename OffT>
-__global__ void __launch_bounds__(kThreads) k_bu(Params<OffT> p, uint32_t depth,
-                                                 const uint32_t* front, uint32_t* next_local) {
+__global__ void __launch_bounds__(kThreads) k_bu(Params<OffT> p, uint32_t* bm0, uint32_t* bm1,
+                                                 uint64_t lo_word, const PartState* st) {
+  if (st->done || st->td) return;
   __shared__ uint32_t s_list[kWarps][kListCap];
   __shared__ uint32_t s_found[kWarps][kGroupWords];
   const unsigned warp = threadIdx.x >> 5;
+  const uint32_t* front = st->fcur ? bm1 : bm0;
+  uint32_t* next_local = (st->fcur ? bm0 : bm1) + lo_word;
   WarpTally t;
-  bu_phase(p, depth, front, next_local, s_list[warp], s_found[warp], t,
+  bu_phase(p, st->depth, front, next_local, s_list[warp], s_found[warp], t,
            &p.ctl->cnt[0].bu_cursor, false);
   warp_flush_tally(&p.ctl->cnt[0], t, false);
 }
 
-__global__ void k_popcount(const uint32_t* __restrict__ bm, uint64_t words, PartState* st) {
+// Distinct size of the gathered next frontier (same value on every rank).
+__global__ void k_popcount(const uint32_t* __restrict__ bm0, const uint32_t* __restrict__ bm1,
+                           uint64_t words, PartState* st) {
+  if (st->done) return;
+  const uint32_t* bm = st->fcur ? bm0 : bm1;
   unsigned long long c = 0;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
        w += (uint64_t)gridDim.x * blockDim.x) {
@@ -319,13 +351,53 @@ __global__ void k_popcount(const uint32_t* __restrict__ bm, uint64_t words, Part
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&st->distinct, c);
 }
 
-__global__ void k_compact(uint32_t* bm, uint64_t words, uint32_t* queue, LevelCnt* cnt,
-                          PartState* st) {
-  compact_bitmap(bm, queue, (uint32_t)words, &cnt->conv_count, false);
+// single_section + decide_direction (kernels.cpp:384-464, :487-513) for one
+// partition: record the level, stop on an empty frontier, else flip the
+// bitmaps, apply the 5 % rule and request the queue compaction for a
+// top-down level.
+__global__ void k_decide(PartState* st, Ctl* ctl, pbfs_level* recs, int policy, double threshold,
+                         unsigned long long n) {
+  if (st->done) return;
+  const unsigned long long produced = st->distinct;
+  LevelCnt* cnt = &ctl->cnt[0];
+  if (st->depth < kPartRecCap) {
+    pbfs_level r{};
+    r.depth = st->depth;
+    r.phase = st->td ? PBFS_TOP_DOWN : PBFS_BOTTOM_UP;
+    r.frontier_size = st->cur_distinct;
+    r.distinct_size = st->cur_distinct;
+    r.edges_examined = cnt->edges;  // this rank's share
+    recs[st->depth] = r;
+  }
+  if (produced == 0) {
+    st->done = 1;
+    return;
+  }
+  const bool next_td = policy == kPolicyTopDown || (double)produced < threshold * (double)n;
+  st->fcur ^= 1u;
+  st->cur_distinct = produced;
+  st->distinct = 0;
+  st->depth += 1;
+  st->td = next_td ? 1u : 0u;
+  st->compact = next_td ? 1u : 0u;
+  ctl->cnt[1].conv_count = 0;
+  // The next level's counters start from zero.
+  LevelCnt z{};
+  ctl->cnt[0] = z;
+}
+
+// Every rank compacts the FULL gathered frontier (gids) into its queue.
+__global__ void k_compact(const uint32_t* bm0, const uint32_t* bm1, uint64_t words,
+                          uint32_t* queue, LevelCnt* cnt, const PartState* st) {
+  if (!st->compact) return;
+  compact_bitmap(const_cast<uint32_t*>(st->fcur ? bm1 : bm0), queue, (uint32_t)words,
+                 &cnt->conv_count, false);
 }
 
 __global__ void k_set_qlen(const LevelCnt* cnt, PartState* st) {
+  if (!st->compact) return;
   st->qlen = cnt->conv_count;
+  st->compact = 0;
 }
 
 __global__ void k_unrelabel(const uint32_t* __restrict__ dist_pi, uint64_t n,
@@ -375,7 +447,9 @@ struct pbfs_part {
   PartState* st = nullptr;
   PartState* st_host = nullptr;  // pinned mirror
   std::vector<void*> allocs;
-  // level state (identical on every rank)
+  pbfs_level* recs = nullptr;    // device, kPartRecCap level records
+  // host mirror of the level state (identical on every rank)
+  uint32_t issued = 0;           // levels enqueued since begin
   uint32_t depth = 0;
   bool td = true;
   int policy = kPolicyFraction;
@@ -672,6 +746,7 @@ pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void*
     return bail(st);
   if ((st = palloc(g, &g->ctl, sizeof(Ctl))) != PBFS_OK) return bail(st);
   if ((st = palloc(g, &g->st, sizeof(PartState))) != PBFS_OK) return bail(st);
+  if ((st = palloc(g, &g->recs, kPartRecCap * sizeof(pbfs_level))) != PBFS_OK) return bail(st);
   if ((e = cudaMallocHost(&g->st_host, sizeof(PartState))) != cudaSuccess)
     return bail(cuda_fail_p(e, "pinned state"));
   PCUDA(cudaMemset(g->ctl, 0, sizeof(Ctl)), "memset");
@@ -748,102 +823,96 @@ pbfs_status pbfs_part_begin(pbfs_part* g, uint32_t source, const pbfs_config* cf
   g->policy = cfg->force_top_down_only ? kPolicyTopDown : kPolicyFraction;
   g->threshold = cfg->hybrid_threshold_fraction;
   g->fcur = 0;
-  g->qcur = 0;
   g->depth = 0;
-  uint32_t spi32 = 0;
-  PCUDA(cudaMemcpy(&spi32, g->gid + source, 4, cudaMemcpyDeviceToHost), "source gid");
-  const uint64_t spi = spi32;
+  g->issued = 0;
+  g->td = true;
   const uint64_t clear_lo = g->shared ? g->lo / 32 : 0;
   const uint64_t clear_words = g->shared ? g->lwords : g->words_total;
-  const bool set_bit = !g->shared || (spi >= g->lo && spi < g->lo + g->nloc);
-  k_begin<<<g->grid, 256, 0, s>>>(g->dist, g->visited, g->mask, g->nloc, g->lwords, g->bm[0],
-                                  g->bm[1], clear_lo, clear_words, spi, g->lo, set_bit,
-                                  g->queue[0], g->st);
-  PCUDA(cudaGetLastError(), "begin");
+  // decide_direction for the seed (kernels.cpp:154-156); the size-fraction
+  // rule does not need the source degree.
+  const bool seed_td = g->policy == kPolicyTopDown || 1.0 < g->threshold * (double)g->n;
   PCUDA(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s), "memset ctl");
-  // decide_direction for the seed (kernels.cpp:154-156); the source degree
-  // is not needed by the size-fraction rule.
-  g->td = g->policy == kPolicyTopDown || 1.0 < g->threshold * (double)g->n;
-  g->cur_distinct = 1;
+  k_begin<<<g->grid, 256, 0, s>>>(g->dist, g->visited, g->mask, g->nloc, g->lwords, g->bm[0],
+                                  g->bm[1], clear_lo, clear_words, g->gid, source, g->lo,
+                                  g->shared, g->queue[0], g->st, seed_td);
+  PCUDA(cudaGetLastError(), "begin");
   return PBFS_OK;
 }
 
+// Enqueues one level's local work; needs no host knowledge of the level's
+// direction (the kernels read it on the device).
 pbfs_status pbfs_part_step(pbfs_part* g, void* stream) {
   if (!g) return fail(PBFS_E_INPUT, "null argument");
   PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
-  PCUDA(cudaMemsetAsync(&g->ctl->cnt[0], 0, sizeof(LevelCnt), s), "memset counters");
-  uint32_t* next = g->bm[g->fcur ^ 1];
-  uint32_t* next_local = next + g->lo / 32;
-  if (g->td) {
-    // Own slice of the next bitmap must be zero before claims mark it.
-    k_clear<<<g->grid, 256, 0, s>>>(next_local, g->lwords);
-    Params<unsigned long long> p = td_params(g);
-    const size_t vbytes = g->lwords * 4;
-    PCUDA(launch_window(k_td_light<unsigned long long>, g->grid, s, g->visited, vbytes, g->persist,
-                        p, g->depth, g->queue[g->qcur], g->st, g->queue[g->qcur ^ 1], next_local),
+  const uint64_t lo_word = g->lo / 32;
+  k_clear<<<g->grid, 256, 0, s>>>(g->bm[0], g->bm[1], lo_word, g->lwords, g->st);
+  Params<unsigned long long> tp = td_params(g);
+  const size_t vbytes = g->lwords * 4;
+  PCUDA(launch_window(k_td_light<unsigned long long>, g->grid, s, g->visited, vbytes, g->persist,
+                      tp, g->queue[0], g->queue[1], g->bm[0], g->bm[1], lo_word,
+                      (const PartState*)g->st),
+        "top-down launch");
+  if (g->col_maxdeg > kHeavyDeg) {
+    PCUDA(launch_window(k_td_heavy<unsigned long long>, g->grid, s, g->visited, vbytes,
+                        g->persist, tp, g->queue[1], g->bm[0], g->bm[1], lo_word,
+                        (const PartState*)g->st),
           "top-down launch");
-    if (g->col_maxdeg > kHeavyDeg) {
-      PCUDA(launch_window(k_td_heavy<unsigned long long>, g->grid, s, g->visited, vbytes,
-                          g->persist, p, g->depth, g->queue[g->qcur ^ 1], next_local),
-            "top-down launch");
-    }
-  } else {
-    Params<unsigned long long> p = bu_params(g);
-    PCUDA(launch_window(k_bu<unsigned long long>, g->grid, s, g->bm[g->fcur], g->words_total * 4,
-                        g->persist, p, g->depth, g->bm[g->fcur], next_local),
-          "bottom-up launch");
   }
-  PCUDA(cudaGetLastError(), "level launch");
+  Params<unsigned long long> bp = bu_params(g);
+  // The frontier bitmap the bottom-up probes: its parity is known here.
+  PCUDA(launch_window(k_bu<unsigned long long>, g->grid, s, g->bm[g->fcur], g->words_total * 4,
+                      g->persist, bp, g->bm[0], g->bm[1], lo_word, (const PartState*)g->st),
+        "bottom-up launch");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_end_level_async(pbfs_part* g, void* stream) {
+  if (!g) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  k_popcount<<<g->grid, 256, 0, s>>>(g->bm[0], g->bm[1], g->words_total, g->st);
+  k_decide<<<1, 1, 0, s>>>(g->st, g->ctl, g->recs, g->policy, g->threshold, g->n);
+  k_compact<<<g->grid, kThreads, 0, s>>>(g->bm[0], g->bm[1], g->words_total, g->queue[0],
+                                         &g->ctl->cnt[1], g->st);
+  k_set_qlen<<<1, 1, 0, s>>>(&g->ctl->cnt[1], g->st);
+  PCUDA(cudaGetLastError(), "level end");
+  g->fcur ^= 1;  // host parity: names the next level's allgather target
+  ++g->issued;
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_poll(pbfs_part* g, void* stream, uint32_t* done, uint32_t* levels) {
+  if (!g || !done) return fail(PBFS_E_INPUT, "null argument");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  unsigned int overflow = 0;
+  PCUDA(cudaMemcpyAsync(g->st_host, g->st, sizeof(PartState), cudaMemcpyDeviceToHost, s), "read");
+  PCUDA(cudaMemcpyAsync(&overflow, &g->ctl->overflow, 4, cudaMemcpyDeviceToHost, s), "read");
+  PCUDA(cudaStreamSynchronize(s), "level");
+  if (overflow) return fail(PBFS_E_CAPACITY, "partition frontier overflow");
+  *done = g->st_host->done;
+  g->depth = g->st_host->depth;
+  g->td = g->st_host->td != 0;
+  if (levels) *levels = g->st_host->depth + (g->st_host->done ? 1u : 0u);
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_part_level_record(pbfs_part* g, uint32_t depth, pbfs_level* rec) {
+  if (!g || !rec) return fail(PBFS_E_INPUT, "null argument");
+  if (depth >= kPartRecCap) return fail(PBFS_E_CAPACITY, "level beyond the record capacity");
+  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PCUDA(cudaMemcpy(rec, g->recs + depth, sizeof(pbfs_level), cudaMemcpyDeviceToHost), "record");
   return PBFS_OK;
 }
 
 pbfs_status pbfs_part_end_level(pbfs_part* g, void* stream, uint32_t* done, pbfs_level* rec) {
   if (!g || !done) return fail(PBFS_E_INPUT, "null argument");
-  PCUDA(cudaSetDevice(g->device), "cudaSetDevice");
-  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
-  uint32_t* next = g->bm[g->fcur ^ 1];
-  // Distinct size of the (allgathered) next frontier: same value on every rank.
-  PCUDA(cudaMemsetAsync(&g->st->distinct, 0, 8, s), "memset");
-  k_popcount<<<g->grid, 256, 0, s>>>(next, g->words_total, g->st);
-  unsigned long long edges = 0;
-  PCUDA(cudaMemcpyAsync(&edges, &g->ctl->cnt[0].edges, 8, cudaMemcpyDeviceToHost, s), "read");
-  PCUDA(cudaMemcpyAsync(g->st_host, g->st, sizeof(PartState), cudaMemcpyDeviceToHost, s), "read");
-  unsigned int overflow = 0;
-  PCUDA(cudaMemcpyAsync(&overflow, &g->ctl->overflow, 4, cudaMemcpyDeviceToHost, s), "read");
-  PCUDA(cudaStreamSynchronize(s), "level");
-  if (overflow) return fail(PBFS_E_CAPACITY, "partition frontier overflow");
-  const unsigned long long produced = g->st_host->distinct;
-  if (rec) {
-    rec->depth = g->depth;
-    rec->phase = g->td ? PBFS_TOP_DOWN : PBFS_BOTTOM_UP;
-    rec->frontier_size = g->cur_distinct;
-    rec->distinct_size = g->cur_distinct;
-    rec->duplicate_count = 0;
-    rec->edges_examined = edges;  // this rank's share
-    rec->flush_events = 0;
-    rec->elapsed_ns = 0;
-  }
-  if (produced == 0) {
-    *done = 1;
-    return PBFS_OK;
-  }
-  *done = 0;
-  const bool next_td = g->policy == kPolicyTopDown ||
-                       (double)produced < g->threshold * (double)g->n;
-  g->fcur ^= 1;  // next becomes the frontier
-  if (next_td) {
-    // Every rank compacts the full frontier (global pi-ids) into its queue.
-    PCUDA(cudaMemsetAsync(&g->ctl->cnt[1], 0, sizeof(LevelCnt), s), "memset");
-    g->qcur = 0;
-    k_compact<<<g->grid, kThreads, 0, s>>>(g->bm[g->fcur], g->words_total, g->queue[0],
-                                           &g->ctl->cnt[1], g->st);
-    k_set_qlen<<<1, 1, 0, s>>>(&g->ctl->cnt[1], g->st);
-    PCUDA(cudaGetLastError(), "compact");
-  }
-  g->td = next_td;
-  g->cur_distinct = produced;
-  ++g->depth;
+  const uint32_t depth = g->issued;
+  pbfs_status st = pbfs_part_end_level_async(g, stream);
+  if (st != PBFS_OK) return st;
+  if ((st = pbfs_part_poll(g, stream, done, nullptr)) != PBFS_OK) return st;
+  if (rec) return pbfs_part_level_record(g, depth, rec);
   return PBFS_OK;
 }
 

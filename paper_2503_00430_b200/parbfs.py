@@ -829,6 +829,24 @@ class PartitionedGraph:
                                              rec.frontier_size, rec.distinct_size,
                                              rec.duplicate_count, rec.edges_examined, 0, 0)
 
+    def end_level_async(self, stream: int = 0) -> None:
+        """Enqueue the level's decision on the device (no sync)."""
+        _check(lib.pbfs_part_end_level_async(self.h, ctypes.c_void_p(stream) if stream else None))
+
+    def poll(self, stream: int = 0):
+        """Synchronise; (done, levels recorded so far)."""
+        done = ctypes.c_uint32()
+        levels = ctypes.c_uint32()
+        _check(lib.pbfs_part_poll(self.h, ctypes.c_void_p(stream) if stream else None,
+                                  ctypes.byref(done), ctypes.byref(levels)))
+        return bool(done.value), int(levels.value)
+
+    def level_record(self, depth: int) -> LevelRecord:
+        rec = L.Level()
+        _check(lib.pbfs_part_level_record(self.h, int(depth), ctypes.byref(rec)))
+        return LevelRecord(rec.depth, TraversalPhase(rec.phase), rec.frontier_size,
+                           rec.distinct_size, rec.duplicate_count, rec.edges_examined, 0, 0)
+
     def sync(self, stream: int = 0) -> None:
         _check(lib.pbfs_part_sync(self.h, ctypes.c_void_p(stream) if stream else None))
 

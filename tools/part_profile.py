@@ -65,7 +65,25 @@ for s in pb.pick_sources(g, args.sources, 1):
                 break
         t_all1.record(stream)
         t_all1.synchronize()
-    print(f"   partitioned x{G}: {t_all0.elapsed_time(t_all1):.3f} ms (host-driven, incl. syncs)")
+    print(f"   partitioned x{G}: {t_all0.elapsed_time(t_all1):.3f} ms (a sync every level)")
+    for look in (4, 8):
+        for rep in range(2):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for p in parts:
+                p.begin(s, cfg, sptr)
+            while True:
+                for _ in range(look):
+                    for p in parts:
+                        p.step(sptr)
+                    for p in parts:
+                        p.end_level_async(sptr)
+                if parts[0].poll(sptr)[0]:
+                    break
+            b.record(stream)
+            b.synchronize()
+        print(f"   partitioned x{G}, {look} levels per poll: {a.elapsed_time(b):.3f} ms")
     for rec, steps, endt in rows:
         print(f"   d={rec.depth} {pb.to_string(rec.phase):9s} step ms per partition "
               f"{[round(x, 3) for x in steps]} end_level {endt:.3f} ms")
