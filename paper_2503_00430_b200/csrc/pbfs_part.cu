@@ -55,15 +55,10 @@ struct Relabel {
   uint32_t k = 0;       // n_pad = 2^k when hashed
   uint32_t hashed = 0;  // 0: identity
   uint64_t mask = 0;
-  uint64_t a = 0, ainv = 0, b = 0, binv = 0;
+  uint64_t a = 0, b = 0;
   uint32_t h = 0;
 };
 
-uint64_t inv_odd(uint64_t a, uint64_t mask) {  // a^-1 mod 2^k (Newton)
-  uint64_t x = a;
-  for (int i = 0; i < 6; ++i) x *= 2 - a * x;
-  return x & mask;
-}
 
 Relabel make_relabel(uint32_t k, bool hashed) {
   Relabel r;
@@ -74,8 +69,6 @@ Relabel make_relabel(uint32_t k, bool hashed) {
   r.b = 0xC2B2AE3D27D4EB4Full & r.mask;
   r.a |= 1;
   r.b |= 1;
-  r.ainv = inv_odd(r.a, r.mask);
-  r.binv = inv_odd(r.b, r.mask);
   r.h = (k + 1) / 2;  // 2h >= k: x ^= x >> h is its own inverse
   return r;
 }
@@ -85,12 +78,6 @@ __host__ __device__ __forceinline__ uint64_t pi_fwd(const Relabel& r, uint64_t v
   uint64_t x = (v * r.a) & r.mask;
   x ^= x >> r.h;
   return (x * r.b) & r.mask;
-}
-__host__ __device__ __forceinline__ uint64_t pi_inv(const Relabel& r, uint64_t y) {
-  if (!r.hashed) return y;
-  uint64_t x = (y * r.binv) & r.mask;
-  x ^= x >> r.h;
-  return (x * r.ainv) & r.mask;
 }
 
 // ---- partition-build kernels ---------------------------------------------------
@@ -441,7 +428,6 @@ struct pbfs_part {
   uint32_t* bm[2] = {nullptr, nullptr};  // full bitmaps (own or shared)
   int fcur = 0;                  // bm[fcur] = current frontier, bm[fcur^1] = next
   uint32_t* queue[2] = {nullptr, nullptr};
-  int qcur = 0;
   HeavyItem* heavy = nullptr;
   Ctl* ctl = nullptr;
   PartState* st = nullptr;
@@ -454,8 +440,6 @@ struct pbfs_part {
   bool td = true;
   int policy = kPolicyFraction;
   double threshold = 0.05;
-  unsigned long long cur_distinct = 1;
-  unsigned long long edges_level = 0;
 };
 
 namespace {
