@@ -573,8 +573,9 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   if ((st = dalloc(g, &g->col, ((m + 15) / 16) * 64 + 64)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->init_mask, wbytes)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->first_nbr, (n + 1) * 4)) != PBFS_OK) return bail(st);
-  // Whole 16-entry groups: the batch path's pack pass reads 64 B at a time.
-  if ((st = dalloc(g, &g->dist, ((n + 15) / 16) * 64)) != PBFS_OK) return bail(st);
+  // Whole 32-entry groups: front_from_dist reads 128 B per bitmap word and
+  // the batch path's pack pass 64 B at a time.
+  if ((st = dalloc(g, &g->dist, ((n + 31) / 32) * 128)) != PBFS_OK) return bail(st);
   // visited | frontier | next bitmaps in one block: the probe-heavy working
   // set (3 n/8 bytes) sits under one persisting L2 access-policy window so
   // the multi-GB `col` stream cannot evict it.
@@ -767,7 +768,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     g->widener.reset(new Widener(std::max(1u, std::thread::hardware_concurrency())));
   }
   if (!g->dist2) {
-    pbfs_status st = dalloc(g, &g->dist2, ((n + 15) / 16) * 64);
+    pbfs_status st = dalloc(g, &g->dist2, ((n + 31) / 32) * 128);
     if (st != PBFS_OK) return st;
   }
   if (g->ctl_host_cap < count) {

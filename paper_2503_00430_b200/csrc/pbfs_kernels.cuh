@@ -486,9 +486,12 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
       winmask |= (uint32_t)won << k;
       if constexpr (C == kClaimBitmap) {
         if (won) p.dist[v[k]] = nd;
-        // Winners also mark the next-frontier bitmap (no-return red), so a
-        // switch to bottom-up needs no separate mark pass.
-        red_or_if(won, &obm[v[k] >> 5], 1u << (v[k] & 31));
+        // Winners mark the next-frontier bitmap (no-return red) where the
+        // caller needs it during the level (partitions exchange it); the
+        // single-GPU engine passes obm = nullptr and rebuilds the bitmap from
+        // dist only when bottom-up follows (front_from_dist): the reds cost
+        // ~7 % of a huge top-down level.
+        red_or_if(won && obm != nullptr, &obm[v[k] >> 5], 1u << (v[k] & 31));
       }
     }
     t.produced += __popc(winmask);
@@ -975,6 +978,32 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
   }
 }
 
+// Top-down -> bottom-up (kernels.cpp:191-213, "clear + mark"): the next
+// frontier is exactly the vertices at distance nd, so its bitmap is one
+// coalesced pass over dist (thread per word, 128 B per thread) instead of a
+// red per discovery during the level. Bits past n stay clear.
+__device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dist, uint32_t nd,
+                                                uint32_t* out, uint32_t words,
+                                                unsigned long long n) {
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       w < words; w += nthreads) {
+    const unsigned long long base = w * 32;
+    uint32_t bits = 0;
+    if (base < n) {
+      const uint4* d4 = reinterpret_cast<const uint4*>(dist + base);  // dist padded to 32
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 a = __ldcs(d4 + q);
+        bits |= (uint32_t)(a.x == nd) << (4 * q) | (uint32_t)(a.y == nd) << (4 * q + 1) |
+                (uint32_t)(a.z == nd) << (4 * q + 2) | (uint32_t)(a.w == nd) << (4 * q + 3);
+      }
+      if (n - base < 32) bits &= (1u << (n - base)) - 1u;
+    }
+    out[w] = bits;
+  }
+}
+
 template <int C, typename OffT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
   __shared__ uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
@@ -1043,10 +1072,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
   unsigned long long t_start = leader ? globaltimer() : 0;
   bar.sync();
 
-  // Bitmap bookkeeping (kClaimBitmap). bm[fcur] holds the latest frontier in
-  // bitmap form; invariant: bm[fcur ^ 1] is all-zero when a top-down level
-  // starts. A top-down level marks its winners into bm[fcur ^ 1] and zeroes
-  // the words of its own input frontier in bm[fcur]; then fcur flips.
+  // Bitmap bookkeeping (kClaimBitmap): fcur flips every level. A bottom-up
+  // level reads bm[fcur] and writes every word of bm[fcur ^ 1]; a top-down
+  // level touches no bitmap but `visited`, and the bitmap of its output is
+  // built from dist only when bottom-up follows.
   uint32_t depth = 0;
   for (;; ++depth) {
     LevelCnt* cnt = &ctl->cnt[depth & 3];
@@ -1074,9 +1103,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
 #endif
     if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
-      uint32_t* mark = C == kClaimBitmap ? p.bm[fcur ^ 1] : nullptr;
-      uint32_t* stale = C == kClaimBitmap ? p.bm[fcur] : nullptr;
-      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, stale);
+      // No next-bitmap marks during the level (see front_from_dist).
+      uint32_t* mark = nullptr;
+      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, nullptr);
       tl_mark(0);
       if (p.max_degree > p.heavy_deg) {
         bar.sync(cnt);
@@ -1158,15 +1187,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       if (qlen > p.qcap) qlen = p.qcap;
       qcur ^= 1;
     } else if (!td && next_td) {
-      // Entering top-down: ascending queue from the produced bitmap
-      // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241); the
-      // stale bitmap is cleared on the way to restore the invariant.
-      compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false,
-                     p.bm[fcur ^ 1], p.force & kForceWideCompact);
+      // Entering top-down: a queue from the produced bitmap
+      // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241).
+      compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false, nullptr,
+                     p.force & kForceWideCompact);
       bar.sync(cnt);
       qlen = snap.conv_count();
+    } else if (C == kClaimBitmap && td && !next_td) {
+      // Entering bottom-up: the frontier bitmap from this level's distances.
+      front_from_dist(p.dist, depth + 1, p.bm[fcur], p.words, p.n);
+      bar.sync();
     }
-    // top-down -> bottom-up: bm[fcur] already holds the marked frontier;
     // bottom-up -> bottom-up: nothing to convert.
     td = next_td;
     cur_raw = raw;
