@@ -192,6 +192,8 @@ struct pbfs_graph {
   uint32_t* visited = nullptr;
   uint32_t* bm[2] = {nullptr, nullptr};
   uint32_t* queue[2] = {nullptr, nullptr};
+  uint4* lq[2] = {nullptr, nullptr};  // latency-mode queues (hub-free graphs only)
+  int lat_grid = 0;                   // latency-mode grid (one CTA per SM)
   HeavyItem* heavy = nullptr;
   Ctl* ctl = nullptr;
   pbfs_level* records = nullptr;
@@ -305,6 +307,14 @@ pbfs_status map_variant(const pbfs_config* c, bool* hybrid_like, Launch* out) {
   }
 }
 
+// Latency mode (pbfs_kernels.cuh: td_phase_latency): the visited-bitmap
+// claim run top-down only on a graph without hubs. PBFS_LATENCY=0 disables it.
+bool latency_mode(const pbfs_graph* g, int claim, int policy) {
+  const char* e = std::getenv("PBFS_LATENCY");
+  const bool off = e && e[0] == '0';
+  return !off && g->lq[0] && claim == kClaimBitmap && policy == kPolicyTopDown;
+}
+
 template <int C, typename OffT>
 cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, int policy,
                          cudaStream_t s, uint32_t* dist, void* pack) {
@@ -320,6 +330,9 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.first_nbr = g->first_nbr;
   p.queue[0] = g->queue[0];
   p.queue[1] = g->queue[1];
+  p.lq[0] = g->lq[0];
+  p.lq[1] = g->lq[1];
+  p.latency = latency_mode(g, C, policy) ? 1 : 0;
   p.heavy = g->heavy;
   p.ctl = g->ctl;
   p.records = g->records;
@@ -342,7 +355,7 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.alpha = cfg->alpha;
   p.beta = cfg->beta;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(g->grid);
+  lc.gridDim = dim3(p.latency ? g->lat_grid : g->grid);
   lc.blockDim = dim3(kThreads);
   lc.dynamicSmemBytes = 0;
   lc.stream = s;
@@ -585,6 +598,11 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   g->bitmap_bytes = 3 * wbytes;
   if ((st = dalloc(g, &g->queue[0], g->qcap * 4)) != PBFS_OK) return bail(st);
   if ((st = dalloc(g, &g->queue[1], g->qcap * 4)) != PBFS_OK) return bail(st);
+  if (g->max_degree <= g->heavy_deg) {
+    // Hub-free graph: 16 B queue entries for the latency-mode top-down path.
+    if ((st = dalloc(g, &g->lq[0], g->qcap * sizeof(uint4))) != PBFS_OK) return bail(st);
+    if ((st = dalloc(g, &g->lq[1], g->qcap * sizeof(uint4))) != PBFS_OK) return bail(st);
+  }
   if ((st = dalloc(g, &g->heavy, std::max<uint64_t>(g->heavy_cap, 1) * sizeof(HeavyItem))) != PBFS_OK)
     return bail(st);
   if ((st = dalloc(g, &g->ctl, sizeof(Ctl))) != PBFS_OK) return bail(st);
@@ -639,6 +657,15 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   }
   if (occ < 1) return bail(fail(PBFS_E_DEVICE, "traversal kernel cannot be resident"));
   g->grid = prop.multiProcessorCount * occ;
+  if (const char* e = std::getenv("PBFS_GRID")) {  // A/B knob: a smaller persistent grid
+    g->grid = std::max(1, std::min(g->grid, std::atoi(e)));
+  }
+  // Latency mode: one CTA per SM halves nothing of a small level's work but
+  // a quarter of its grid-barrier time (tools/ubench_barrier.cu: 1.5 vs 2.0 us).
+  g->lat_grid = prop.multiProcessorCount;
+  if (const char* e = std::getenv("PBFS_LATENCY_GRID")) {
+    g->lat_grid = std::max(1, std::min(g->grid, std::atoi(e)));
+  }
   // Persisting L2 set-aside for the bitmap block (process-wide device limit;
   // only ever raised). PBFS_NO_L2_PERSIST=1 disables it for A/B runs.
   const char* no_persist = std::getenv("PBFS_NO_L2_PERSIST");

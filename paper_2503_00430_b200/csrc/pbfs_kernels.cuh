@@ -203,6 +203,10 @@ struct Params {
   uint32_t small_chunks;  // heavy_cap covers kSmallChunkLog2 items on small frontiers
   uint32_t force;         // kForce* test hooks (PBFS_FORCE_MODES at graph creation)
   void* pack;             // optional: narrow copy of dist for the host transfer (see pack_width)
+  // Latency mode (deep, hub-free graphs run top-down only, e.g. config 3's
+  // mesh): 16 B queue entries {v, degree, row offset lo, hi}, see td_phase_latency.
+  uint4* lq[2];
+  int latency;
   uint32_t source;
   int policy;
   int validate;
@@ -656,6 +660,147 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
   (void)cnt;
 }
 
+// ---- latency mode ---------------------------------------------------------------
+// A deep graph (config 3: ~3900 levels of ~4 K vertices) is bound by one
+// level's dependent chain, not by bytes: queue -> rowptr -> col -> probe ->
+// claim -> flush, then the barrier. On a hub-free graph run top-down only the
+// chain loses two round trips: queue entries carry the row range {v, degree,
+// beg} (the winner loads rowptr in the shadow of its claim atomic, for every
+// live slot at once), and the claim is the atom.or alone (its returned word
+// settles the race; the L1 probe only saves atomics when most targets are
+// visited, which costs an extra round trip here).
+
+// Per-warp buffer of 16 B entries in the warp's s_list slice.
+struct WarpPush4 {
+  uint4* buf;  // kPushBuf / 4 entries
+  int count;   // warp-uniform
+  __device__ __forceinline__ void flush(uint4* out, unsigned long long* counter,
+                                        unsigned long long cap, unsigned int* overflow) {
+    __syncwarp();
+    if (count) {
+      unsigned long long base = 0;
+      if (lane_id() == 0) base = atomicAdd(counter, (unsigned long long)count);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + count <= cap) {
+        for (int i = lane_id(); i < count; i += 32) out[base + i] = buf[i];
+      } else if (lane_id() == 0) {
+        atomicExch(overflow, 1u);
+      }
+    }
+    count = 0;
+    __syncwarp();
+  }
+};
+
+template <int K, typename OffT>
+__device__ __forceinline__ void claim_latency(const Params<OffT>& p, uint32_t nd,
+                                              const uint32_t (&v)[K], uint32_t okm, uint4* qout,
+                                              WarpPush4& wp, LevelCnt* cnt, WarpTally& t) {
+  constexpr int kCap = kPushBuf / 4;
+  uint32_t w[K];
+  OffT b0[K], b1[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t bit = 1u << (v[k] & 31);
+    w[k] = atom_or_if((okm >> k) & 1u, &p.visited[v[k] >> 5], bit, 0xffffffffu);
+    b0[k] = ld_stream(&p.rowptr[v[k]]);  // dead slots hold a valid id
+    b1[k] = ld_stream(&p.rowptr[v[k] + 1]);
+  }
+  uint32_t winmask = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool won = !(w[k] & (1u << (v[k] & 31)));
+    winmask |= (uint32_t)won << k;
+    if (won) p.dist[v[k]] = nd;
+  }
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = lane_id();
+  const uint32_t c = __popc(winmask);
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t x = __shfl_up_sync(FULL, incl, o);
+    if (lane >= (unsigned)o) incl += x;
+  }
+  const int total = (int)__shfl_sync(FULL, incl, 31);
+  if (total == 0) return;
+  t.produced += c;
+  if (wp.count + total > kCap) wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+  uint32_t pos = wp.count + incl - c;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if ((winmask >> k) & 1u) {
+      const unsigned long long b = (unsigned long long)b0[k];
+      wp.buf[pos++] = make_uint4(v[k], (uint32_t)(b1[k] - b0[k]), (uint32_t)b, (uint32_t)(b >> 32));
+    }
+  }
+  wp.count += total;
+}
+
+// Top-down level of latency mode: 32 queue entries per warp slice (static
+// first slice, then the cursor), warp-cooperative expansion as
+// td_light_batch; no hub items (the graph has none).
+template <typename OffT>
+__device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const uint4* qin,
+                                 unsigned long long qlen, uint4* qout, WarpPush4& wp,
+                                 LevelCnt* cnt, WarpTally& t) {
+  // 4 slots: 32 vertices of a hub-free deep graph (degree ~4) fit one batch,
+  // and the speculative offsets of 8 slots would spill.
+  constexpr int K = 4;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = lane_id();
+  const uint32_t nd = depth + 1;
+  const unsigned warps_total = gridDim.x * kWarps;
+  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
+  while (base < qlen) {
+    const unsigned long long i = base + lane;
+    uint32_t deg = 0;
+    unsigned long long beg = 0;
+    if (i < qlen) {
+      const uint4 q = qin[i];
+      deg = q.y;
+      beg = (unsigned long long)q.z | ((unsigned long long)q.w << 32);
+    }
+    t.edges += deg;
+    uint32_t incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (unsigned)o) incl += x;
+    }
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    const uint32_t excl = incl - deg;
+    if (total) {
+      const unsigned nz = __ballot_sync(FULL, deg != 0);
+      const unsigned long long b0 = __shfl_sync(FULL, beg, __ffs(nz) - 1);
+      for (uint32_t e0 = 0; e0 < total; e0 += 32 * K) {
+        uint32_t v[K];
+        uint32_t okm = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t e = e0 + 32 * k + lane;
+          int j = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t x = __shfl_sync(FULL, incl, j + step - 1);
+            if (x <= e) j += step;
+          }
+          const unsigned long long ob = __shfl_sync(FULL, beg, j);
+          const uint32_t oex = __shfl_sync(FULL, excl, j);
+          const bool ok = e < total;
+          okm |= (uint32_t)ok << k;
+          v[k] = ld_stream(&p.col[ok ? ob + (e - oex) : b0]);
+        }
+        claim_latency<K>(p, nd, v, okm, qout, wp, cnt, t);
+      }
+    }
+    if (qlen <= (unsigned long long)warps_total * 32) break;
+    unsigned int nb = 0;
+    if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
+    base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
+  }
+}
+
 // Bottom-up over all vertices (kernels.cpp:340-382), per warp task of one
 // 32-word group (one visited word per lane), or of kBuSparseGroups groups
 // with all loads in flight when few vertices are left unvisited (settled
@@ -1006,7 +1151,7 @@ __device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dis
 
 template <int C, typename OffT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
-  __shared__ uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
+  __shared__ __align__(16) uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
   __shared__ uint32_t s_found[kWarps][kGroupWords];
   __shared__ unsigned long long s_snap[8];  // level-counter snapshot (GridBarrier)
   const unsigned warp = threadIdx.x >> 5;
@@ -1040,6 +1185,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     }
     if (leader) {
       p.queue[0][0] = src;
+      if (p.latency) {
+        const unsigned long long b = (unsigned long long)p.rowptr[src];
+        p.lq[0][0] = make_uint4(src, (uint32_t)(p.rowptr[src + 1] - p.rowptr[src]), (uint32_t)b,
+                                (uint32_t)(b >> 32));
+      }
       for (int s = 0; s < 4; ++s) {
         LevelCnt z{};
         ctl->cnt[s] = z;
@@ -1101,7 +1251,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
 #else
     auto tl_mark = [](int) {};
 #endif
-    if (td) {
+    if (td && p.latency) {
+      WarpPush4 wp4{reinterpret_cast<uint4*>(s_list[warp]), 0};
+      td_phase_latency(p, depth, p.lq[qcur], qlen, p.lq[qcur ^ 1], wp4, cnt, t);
+      wp4.flush(p.lq[qcur ^ 1], &cnt->raw, p.qcap, &ctl->overflow);
+      tl_mark(0);
+    } else if (td) {
       uint32_t* qout = p.queue[qcur ^ 1];
       // No next-bitmap marks during the level (see front_from_dist).
       uint32_t* mark = nullptr;

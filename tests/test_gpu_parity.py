@@ -367,3 +367,30 @@ def test_time_run_checks_every_run(port):
         return r
     with pytest.raises(pb.CorrectnessError, match="vertex 5"):
         pb.time_run(g, 0, pb.KernelConfig(variant=V.Hybrid), 1, 0, broken, want)
+
+
+@pytest.mark.parametrize("offset_bytes", [4, 8])
+def test_latency_mode_matches_the_general_top_down(offset_bytes, port, monkeypatch):
+    # Hub-free graphs run top-down only take the latency-mode kernel path
+    # (16 B queue entries with row ranges, atom.or-only claims, one CTA per
+    # SM); it must give the oracle's distances and the general path's trace.
+    graphs = [pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Mesh, seed=3, mesh_side=96,
+                                           drop_self_loops=True)),
+              make_path(5000), make_circulant(4000, [1, 7, 33]),
+              random_graph(3000, 6000, 5)]
+    for g in graphs:
+        assert int(g.degrees().max()) <= 128
+        srcs = [int(x) for x in pb.pick_sources(g, 3, 2)]
+        recs = {}
+        for lat in ("1", "0"):
+            monkeypatch.setenv("PBFS_LATENCY", lat)
+            dg = g.device(0, offset_bytes)
+            for s in srcs:
+                want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+                r = dg.bfs(s, pb.KernelConfig(variant=V.Hybrid, force_top_down_only=True))
+                assert np.array_equal(r.distances, want), (lat, s)
+                recs[lat, s] = [(x.depth, x.phase, x.frontier_size, x.distinct_size,
+                                 x.edges_examined) for x in r.trace.records]
+            g.release_device()
+        for s in srcs:
+            assert recs["1", s] == recs["0", s]
