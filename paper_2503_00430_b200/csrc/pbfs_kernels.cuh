@@ -111,7 +111,7 @@ constexpr int kListCap = 512;        // bottom-up: unvisited ids listed per roun
 #define PBFS_BU_WIN 8
 #endif
 constexpr int kBuWin = PBFS_BU_WIN;        // bottom-up scan window (8 or 16 entries)
-static_assert(kBuWin == 8 || kBuWin == 16, "PBFS_BU_WIN must be 8 or 16");
+static_assert(kBuWin == 4 || kBuWin == 8 || kBuWin == 16, "PBFS_BU_WIN must be 4, 8 or 16");
 constexpr int kBuSlots = PBFS_BU_SLOTS;    // unvisited vertices per lane in flight
 // 32-word groups per bottom-up task: 1 (finest balance), or kBuSparseGroups
 // on a sparse level (few unvisited vertices left), where a task is mostly
@@ -565,11 +565,16 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
   const unsigned warps_total = gridDim.x * kWarps;
-  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
+  // Slice width: 32 frontier vertices per warp, fewer on a frontier smaller
+  // than one full slice per warp, so its edges spread over more warps instead
+  // of queueing up as batches (each a dependent round-trip chain) in a few.
+  uint32_t W = 32;
+  while (W > 1 && (unsigned long long)warps_total * (W / 2) >= qlen) W /= 2;
+  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * W;
   while (base < qlen) {
     const unsigned long long i = base + lane;
     OffT beg = 0, end = 0;
-    if (i < qlen) {
+    if (lane < W && i < qlen) {
       const uint32_t u = qin[i];
       beg = __ldg(&p.rowptr[u]);
       end = __ldg(&p.rowptr[u + 1]);
@@ -613,7 +618,7 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
     td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t, obm);
     // The static first slices cover small frontiers entirely: no cursor
     // round trip at all (the common case on deep, narrow graphs).
-    if (qlen <= (unsigned long long)warps_total * 32) break;
+    if (qlen <= (unsigned long long)warps_total * W) break;
     unsigned int nb = 0;
     if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
     base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
