@@ -35,6 +35,23 @@ using namespace pbfs::dev;
 namespace {
 
 constexpr uint64_t kPackMinVertices = uint64_t{1} << 25;
+// Narrow-transfer slots of pbfs_bfs_batch: traversal i may run while the
+// widening of i - 1 .. i - (slots - 1) is still queued on the host, so the
+// host-bound widening (~2.3 ms per RMAT-26 array with the transfers landing
+// alongside) and the traversal time (0.8 - 5.8 ms per source) average out
+// over sources instead of pairwise (RMAT-26 e2e: 2 slots 317, 4 slots 346,
+// 6 or 8 no better).
+constexpr int kMaxBatchSlots = 8;
+constexpr int kBatchSlots = 4;
+
+// Host threads of the widening pool (PBFS_WIDEN_THREADS overrides for A/B runs).
+unsigned widen_threads() {
+  // Every hardware thread (RMAT-26 e2e, 16-core host: 16 threads 346, 14
+  // threads 343 GTEPS -- within run-to-run noise).
+  unsigned t = std::max(1u, std::thread::hardware_concurrency());
+  if (const char* e = std::getenv("PBFS_WIDEN_THREADS")) t = std::max(1, std::atoi(e));
+  return t;
+}
 
 // Host-side widening of packed distances (1 or 2 B per vertex, all-ones =
 // unreached) into the caller's uint32 arrays, on a persistent pool. Jobs are
@@ -212,9 +229,10 @@ struct pbfs_graph {
   // pbfs_bfs_batch state, created on first use.
   uint32_t* dist2 = nullptr;
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t kern_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
-  void* pack[2] = {nullptr, nullptr};      // device: packed distances (<= 2 B per vertex)
-  void* stage[2] = {nullptr, nullptr};     // pinned host: their landing buffers
+  int batch_slots = 0;
+  cudaEvent_t kern_done[kMaxBatchSlots] = {}, copy_done[kMaxBatchSlots] = {};
+  void* pack[kMaxBatchSlots] = {};   // device: packed distances (<= 2 B per vertex)
+  void* stage[kMaxBatchSlots] = {};  // pinned host: their landing buffers
   std::unique_ptr<Widener> widener;
   Ctl* ctl_host = nullptr;  // pinned, ctl_host_cap entries
   uint32_t ctl_host_cap = 0;
@@ -259,7 +277,7 @@ void release(pbfs_graph* g) {
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   for (void* h : g->stage) if (h) cudaFreeHost(h);
   for (cudaEvent_t e : g->run_ev) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kMaxBatchSlots; ++i) {
     if (g->kern_done[i]) cudaEventDestroy(g->kern_done[i]);
     if (g->copy_done[i]) cudaEventDestroy(g->copy_done[i]);
   }
@@ -782,17 +800,21 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   const uint64_t n = g->n;
   if (!g->copy_stream) {
     PBFS_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    for (int i = 0; i < 2; ++i) {
+    g->batch_slots = kBatchSlots;
+    if (const char* es = std::getenv("PBFS_BATCH_SLOTS")) {
+      g->batch_slots = std::max(2, std::min(kMaxBatchSlots, std::atoi(es)));
+    }
+    for (int i = 0; i < g->batch_slots; ++i) {
       PBFS_CUDA(cudaEventCreateWithFlags(&g->kern_done[i], cudaEventDisableTiming), "cudaEventCreate");
       PBFS_CUDA(cudaEventCreateWithFlags(&g->copy_done[i], cudaEventDisableTiming), "cudaEventCreate");
     }
     const uint64_t pbytes = ((n + 15) / 16) * 32;  // 2 B per vertex, whole 16-vertex groups
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < g->batch_slots; ++i) {
       pbfs_status st = dalloc(g, &g->pack[i], pbytes);
       if (st != PBFS_OK) return st;
       PBFS_CUDA(cudaHostAlloc(&g->stage[i], pbytes, cudaHostAllocDefault), "pinned staging");
     }
-    g->widener.reset(new Widener(std::max(1u, std::thread::hardware_concurrency())));
+    g->widener.reset(new Widener(widen_threads()));
   }
   if (!g->dist2) {
     pbfs_status st = dalloc(g, &g->dist2, ((n + 31) / 32) * 128);
@@ -811,7 +833,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     PBFS_CUDA(cudaEventCreate(&ev), "cudaEventCreate");
     g->run_ev.push_back(ev);
   }
-  // Pipeline per source i (slot = i & 1):
+  // Pipeline per source i (slot = i % S; dist buffer i & 1):
   //   compute stream: traversal i into dist/pack[slot] (+ a narrow copy of
   //                   the distances at the end), control snapshot;
   //   copy stream:    pack[slot] -> pinned stage[slot] (1 or 2 B/vertex,
@@ -825,17 +847,20 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   // and the host-side widening (measured: RMAT-26 4.84 -> 3.47 ms per source;
   // ER-24 and smaller are faster with the plain copy).
   const bool packed = n >= kPackMinVertices || (g->force & kForcePack);
+  // Plain copies read the dist buffers themselves: two slots.
+  const uint32_t S = packed ? static_cast<uint32_t>(g->batch_slots) : 2u;
+  std::vector<uint8_t> reads_dist(count, packed ? 0 : 1);  // transfer j copies buf[j & 1]
   Widener& wd = *g->widener;
   wd.reset();
   std::vector<Widener::Job> jobs(count);
   std::unordered_map<const uint32_t*, int64_t> last_use;  // output buffer -> last job writing it
   auto finish = [&](uint32_t j) -> cudaError_t {
-    const int slot = j & 1;
+    const uint32_t slot = j % S;
     cudaError_t ce;
     if (!packed) {
       // Plain 4 B/vertex copy, stream-ordered: no host wait at all.
       if ((ce = cudaStreamWaitEvent(g->copy_stream, g->kern_done[slot], 0)) != cudaSuccess) return ce;
-      if ((ce = cudaMemcpyAsync(dist_host[j], buf[slot], n * 4, cudaMemcpyDeviceToHost,
+      if ((ce = cudaMemcpyAsync(dist_host[j], buf[j & 1], n * 4, cudaMemcpyDeviceToHost,
                                 g->copy_stream)) != cudaSuccess) return ce;
       return cudaEventRecord(g->copy_done[slot], g->copy_stream);
     }
@@ -845,11 +870,12 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     const uint32_t width = packed ? pack_width(c.levels) : 4u;
     Widener::Job& job = jobs[j];
     job = Widener::Job{g->stage[slot], dist_host[j], n, width < 4 ? width : 0, j, &wd};
-    // stage[slot] was last read by job j-2; dist_host[j] may alias an earlier
-    // output (rotating buffers): wait for exactly those jobs, not the queue.
-    int64_t need = j >= 2 ? static_cast<int64_t>(j) - 2 : -1;
+    // stage[slot] was last read by job j-S. dist_host[j] may alias an earlier
+    // output (rotating buffers): the pool runs jobs in order, so only a DMA
+    // straight into dist_host (the 4 B fallback) waits for that job.
+    int64_t need = j >= S ? static_cast<int64_t>(j) - S : -1;
     auto it = last_use.find(dist_host[j]);
-    if (it != last_use.end()) need = std::max<int64_t>(need, it->second);
+    if (width >= 4 && it != last_use.end()) need = std::max<int64_t>(need, it->second);
     if (need >= 0) wd.wait(static_cast<uint64_t>(need));
     last_use[dist_host[j]] = j;
     if ((ce = cudaStreamWaitEvent(g->copy_stream, g->kern_done[slot], 0)) != cudaSuccess) return ce;
@@ -857,7 +883,8 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
       ce = cudaMemcpyAsync(g->stage[slot], g->pack[slot], n * width, cudaMemcpyDeviceToHost,
                            g->copy_stream);
     } else {
-      ce = cudaMemcpyAsync(dist_host[j], buf[slot], n * 4, cudaMemcpyDeviceToHost, g->copy_stream);
+      reads_dist[j] = 1;  // > 65534 levels: the full 4 B copy of the dist buffer
+      ce = cudaMemcpyAsync(dist_host[j], buf[j & 1], n * 4, cudaMemcpyDeviceToHost, g->copy_stream);
     }
     if (ce != cudaSuccess) return ce;
     if ((ce = cudaLaunchHostFunc(g->copy_stream, Widener::submit_cb, &job)) != cudaSuccess) return ce;
@@ -865,11 +892,14 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   };
   for (uint32_t i = 0; i <= count; ++i) {
     if (i < count) {
-      const int slot = i & 1;
-      // pack/dist[slot] are free once transfer i-2 has landed.
-      if (i >= 2 && (e = cudaStreamWaitEvent(g->stream, g->copy_done[slot], 0)) != cudaSuccess) break;
+      const uint32_t slot = i % S;
+      // pack/stage[slot] are free once transfer i-S has landed; dist buffer
+      // i & 1 once transfer i-2 has, if that transfer read it.
+      if (i >= S && (e = cudaStreamWaitEvent(g->stream, g->copy_done[slot], 0)) != cudaSuccess) break;
+      if (i >= 2 && S > 2 && reads_dist[i - 2] &&
+          (e = cudaStreamWaitEvent(g->stream, g->copy_done[(i - 2) % S], 0)) != cudaSuccess) break;
       if ((e = cudaEventRecord(g->run_ev[2 * i], g->stream)) != cudaSuccess) break;
-      if ((e = launch(g, sources[i], cfg, l, g->stream, buf[slot],
+      if ((e = launch(g, sources[i], cfg, l, g->stream, buf[i & 1],
                       packed ? g->pack[slot] : nullptr)) != cudaSuccess) {
         g->poisoned = true;
         break;
@@ -888,7 +918,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   if (e != cudaSuccess || e1 != cudaSuccess || e2 != cudaSuccess) {
     g->poisoned = true;
     // Jobs whose callbacks ran may still be widening: drain the pool first.
-    g->widener.reset(new Widener(std::max(1u, std::thread::hardware_concurrency())));
+    g->widener.reset(new Widener(widen_threads()));
     return cuda_fail(e != cudaSuccess ? e : e1 != cudaSuccess ? e1 : e2, "traversal batch");
   }
   // The handle's dist keeps meaning "the last traversal" (device_dist, component).

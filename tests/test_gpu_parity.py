@@ -279,12 +279,15 @@ def test_async_api_and_device_component(port):
     assert (nr, ar) == port.component(g.row_offsets, want)
 
 
-@pytest.mark.parametrize("force", ["0", "8"], ids=["plain", "packed"])
-def test_batch_api_overlapped_copies(force, port, monkeypatch):
-    # pbfs_bfs_batch: distances of source i land in outs[i] while i+1 runs;
-    # "packed" forces the narrow 1/2 B transfers + host widening that the
-    # library uses from 2^25 vertices up.
+@pytest.mark.parametrize("force,slots", [("0", "4"), ("8", "4"), ("8", "2"), ("8", "8")],
+                         ids=["plain", "packed", "packed2", "packed8"])
+def test_batch_api_overlapped_copies(force, slots, port, monkeypatch):
+    # pbfs_bfs_batch: distances of source i land in outs[i] while later
+    # traversals run; "packed" forces the narrow 1/2 B transfers + host
+    # widening that the library uses from 2^25 vertices up, with 2, 4 (the
+    # default) or 8 transfer slots in flight.
     monkeypatch.setenv("PBFS_FORCE_MODES", force)
+    monkeypatch.setenv("PBFS_BATCH_SLOTS", slots)
     g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 3,
                                      drop_self_loops=True))
     dg = g.device(0, 8)
