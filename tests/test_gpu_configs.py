@@ -101,3 +101,33 @@ def test_config4_rmat26_properties():
     for s in pb.pick_sources(g, 2, 1):
         r = dg.bfs(int(s), cfg)
         bfs_properties(g, r.distances, int(s))
+
+
+@pytest.mark.skipif(os.environ.get("PBFS_TEST_LARGE") != "1", reason="set PBFS_TEST_LARGE=1")
+@pytest.mark.parametrize("name", ["rmat26", "er24", "mesh4096"])
+def test_large_configs_all_64_sources_bit_exact(name, port):
+    # Every one of the bench's 64 seeded sources, bit-exact against the
+    # reference's own parbfs::bfs_hybrid (oracle/_ref, all host threads) on
+    # RMAT-26, against the C port's bfs_serial on ER-24 and the mesh; the
+    # per-level phases and distinct frontier sizes equal the reference's.
+    import oracle
+    g, offb = config_graph(name)
+    dg = g.device(0, offb)
+    cfg = dispatch_config(g)
+    srcs = [int(s) for s in pb.pick_sources(g, 64, 1)]
+    rg = None
+    if name == "rmat26":
+        assert oracle.ref_available()
+        ref = oracle.ref()
+        rg = ref.from_csr(g.row_offsets.astype(np.uint64, copy=False), g.column_indices, True)
+    for i, s in enumerate(srcs):
+        r = dg.bfs(s, cfg)
+        if rg is not None:
+            want, recs, _ = ref.run(rg, s, 3, workers=os.cpu_count() or 1,
+                                    force_td=cfg.force_top_down_only)
+            assert [(x.depth, int(x.phase), x.distinct_size) for x in r.trace.records] == \
+                [(x["depth"], x["phase"], x["distinct_size"]) for x in recs], (name, s)
+        else:
+            want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+        assert np.array_equal(r.distances, want), (name, i, s)
+    g.release_device()
