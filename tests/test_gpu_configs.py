@@ -46,8 +46,8 @@ def config_graph(name):
     if name == "mesh4096":
         return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Mesh, seed=1, mesh_side=4096,
                                             drop_self_loops=True)), 8
-    if name == "rmat26":
-        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 26, 16, 1,
+    if name in ("rmat26", "rmat28"):
+        return pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, int(name[4:]), 16, 1,
                                             drop_self_loops=True)), 8
     raise KeyError(name)
 
@@ -104,19 +104,22 @@ def test_config4_rmat26_properties():
 
 
 @pytest.mark.skipif(os.environ.get("PBFS_TEST_LARGE") != "1", reason="set PBFS_TEST_LARGE=1")
-@pytest.mark.parametrize("name", ["rmat26", "er24", "mesh4096"])
+@pytest.mark.parametrize("name", ["rmat26", "er24", "mesh4096", "rmat28"])
 def test_large_configs_all_64_sources_bit_exact(name, port):
-    # Every one of the bench's 64 seeded sources, bit-exact against the
-    # reference's own parbfs::bfs_hybrid (oracle/_ref, all host threads) on
-    # RMAT-26, against the C port's bfs_serial on ER-24 and the mesh; the
-    # per-level phases and distinct frontier sizes equal the reference's.
+    # Every one of the bench's 64 seeded sources (the first 8 on RMAT-28),
+    # bit-exact against the reference's own parbfs::bfs_hybrid (oracle/_ref,
+    # all host threads) on RMAT-26/28, against the C port's bfs_serial on
+    # ER-24 and the mesh; the per-level phases and distinct frontier sizes
+    # equal the reference's.
     import oracle
     g, offb = config_graph(name)
     dg = g.device(0, offb)
     cfg = dispatch_config(g)
     srcs = [int(s) for s in pb.pick_sources(g, 64, 1)]
+    if name == "rmat28":
+        srcs = srcs[:8]
     rg = None
-    if name == "rmat26":
+    if name.startswith("rmat2"):
         assert oracle.ref_available()
         ref = oracle.ref()
         rg = ref.from_csr(g.row_offsets.astype(np.uint64, copy=False), g.column_indices, True)
