@@ -1132,15 +1132,19 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
 // frontier is exactly the vertices at distance nd, so its bitmap is one
 // coalesced pass over dist (thread per word, 128 B per thread) instead of a
 // red per discovery during the level. Bits past n stay clear.
+// Words without a reached vertex (visited bits all pre-set isolated ones) need
+// no dist read at all: on RMAT most high-id words are all isolated.
 __device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dist, uint32_t nd,
                                                 uint32_t* out, uint32_t words,
-                                                unsigned long long n) {
+                                                unsigned long long n, const uint32_t* visited,
+                                                const uint32_t* init_mask) {
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        w < words; w += nthreads) {
     const unsigned long long base = w * 32;
     uint32_t bits = 0;
-    if (base < n) {
+    const uint32_t reached = __ldcg(&visited[w]) & ~__ldg(&init_mask[w]);
+    if (base < n && reached) {
       const uint4* d4 = reinterpret_cast<const uint4*>(dist + base);  // dist padded to 32
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -1148,7 +1152,7 @@ __device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dis
         bits |= (uint32_t)(a.x == nd) << (4 * q) | (uint32_t)(a.y == nd) << (4 * q + 1) |
                 (uint32_t)(a.z == nd) << (4 * q + 2) | (uint32_t)(a.w == nd) << (4 * q + 3);
       }
-      if (n - base < 32) bits &= (1u << (n - base)) - 1u;
+      bits &= reached;
     }
     out[w] = bits;
   }
@@ -1355,7 +1359,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       qlen = snap.conv_count();
     } else if (C == kClaimBitmap && td && !next_td) {
       // Entering bottom-up: the frontier bitmap from this level's distances.
-      front_from_dist(p.dist, depth + 1, p.bm[fcur], p.words, p.n);
+      front_from_dist(p.dist, depth + 1, p.bm[fcur], p.words, p.n, p.visited, p.init_mask);
       bar.sync();
     }
     // bottom-up -> bottom-up: nothing to convert.
