@@ -419,9 +419,14 @@ int occupancy_for(int claim) {
   const void* fn = claim == kClaimCas     ? reinterpret_cast<const void*>(&bfs_persistent<kClaimCas, OffT>)
                    : claim == kClaimPlain ? reinterpret_cast<const void*>(&bfs_persistent<kClaimPlain, OffT>)
                                           : reinterpret_cast<const void*>(&bfs_persistent<kClaimBitmap, OffT>);
-  // Smallest shared-memory carveout that fits the resident CTAs: the rest of
-  // the 228 KB stays L1, which caches the frozen visited-bitmap probes.
-  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
+  // Smallest shared-memory carveout that fits kMinBlocks resident CTAs: the
+  // rest of the SM's 256 KB stays L1, which caches the visited-bitmap probes
+  // (profiles/r01_ab.txt: 16 KB more per CTA, L1 192 -> 124 KB, cost 17 %).
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  const size_t per_sm = static_cast<size_t>(kMinBlocks) * (fa.sharedSizeBytes + 1024);
+  const int pct = static_cast<int>((per_sm * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0);
   return blocks;
 }

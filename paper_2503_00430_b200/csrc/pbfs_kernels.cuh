@@ -101,9 +101,16 @@ constexpr uint32_t kForceWideCompact = 2;  // 8-words-per-lane compaction
 constexpr uint32_t kForceBigSplit = 4;     // the >= 2^30-arc hub split
 constexpr uint32_t kForcePack = 8;         // pbfs_bfs_batch's narrow transfers at any size
 constexpr uint32_t kSmallChunkLog2 = PBFS_SMALL_CHUNK_LOG2;
-constexpr int kPushBuf = 512;        // per-warp discovery buffer (entries)
+// Per-warp shared-memory buffers: discovery buffer (top-down) / unvisited-id
+// list (bottom-up), same storage. Their size sets the CTA's shared memory and
+// with it the L1 left for the probes (PBFS_LIST_CAP A/B knob).
+#ifndef PBFS_LIST_CAP
+#define PBFS_LIST_CAP 512
+#endif
+constexpr int kPushBuf = PBFS_LIST_CAP;  // per-warp discovery buffer (entries)
 constexpr int kGroupWords = 32;      // bitmap words per warp group (one per lane)
-constexpr int kListCap = 512;        // bottom-up: unvisited ids listed per round
+constexpr int kListCap = PBFS_LIST_CAP;  // bottom-up: unvisited ids listed per round
+static_assert(kPushBuf >= 32 * PBFS_SLOTS, "a top-down batch must fit the discovery buffer");
 #ifndef PBFS_BU_SLOTS
 #define PBFS_BU_SLOTS 4
 #endif
@@ -720,26 +727,33 @@ __device__ __forceinline__ void claim_latency(const Params<OffT>& p, uint32_t nd
   }
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
-  const uint32_t c = __popc(winmask);
-  uint32_t incl = c;
+  // Appended in halves of K / 2 slots, so a half's winners (<= 16 K) always
+  // fit the kPushBuf / 4-entry buffer after a flush.
+  static_assert(kCap >= 16 * K, "latency-mode discovery buffer");
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t x = __shfl_up_sync(FULL, incl, o);
-    if (lane >= (unsigned)o) incl += x;
-  }
-  const int total = (int)__shfl_sync(FULL, incl, 31);
-  if (total == 0) return;
-  t.produced += c;
-  if (wp.count + total > kCap) wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
-  uint32_t pos = wp.count + incl - c;
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t hm = (winmask >> (h * K / 2)) & ((1u << (K / 2)) - 1u);
+    const uint32_t c = __popc(hm);
+    uint32_t incl = c;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if ((winmask >> k) & 1u) {
-      const unsigned long long b = (unsigned long long)b0[k];
-      wp.buf[pos++] = make_uint4(v[k], (uint32_t)(b1[k] - b0[k]), (uint32_t)b, (uint32_t)(b >> 32));
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (unsigned)o) incl += x;
     }
+    const int total = (int)__shfl_sync(FULL, incl, 31);
+    if (total == 0) continue;
+    t.produced += c;
+    if (wp.count + total > kCap) wp.flush(qout, &cnt->raw, p.qcap, &p.ctl->overflow);
+    uint32_t pos = wp.count + incl - c;
+#pragma unroll
+    for (int k = h * K / 2; k < (h + 1) * K / 2; ++k) {
+      if ((winmask >> k) & 1u) {
+        const unsigned long long b = (unsigned long long)b0[k];
+        wp.buf[pos++] = make_uint4(v[k], (uint32_t)(b1[k] - b0[k]), (uint32_t)b, (uint32_t)(b >> 32));
+      }
+    }
+    wp.count += total;
   }
-  wp.count += total;
 }
 
 // Top-down level of latency mode: 32 queue entries per warp slice (static
