@@ -90,10 +90,15 @@ def build_graph(name: str):
     return g
 
 
+# --variant: the kernel the GPU arm runs (the reference's KernelVariant names;
+# "hybrid" -- the paper's 5 % frontier switch -- is the headline).
+VARIANT = os.environ.get("PBFS_BENCH_VARIANT", "hybrid")
+
+
 def kernel_config(graph):
     import paper_2503_00430_b200 as pb
     stats = pb.compute_stats(graph)
-    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid)
+    cfg = pb.KernelConfig(variant=pb.parse_kernel_variant(VARIANT))
     # run_bfs's category dispatcher (kernels.cpp:657-662)
     if stats.category == pb.GraphCategory.LargeDiameter:
         cfg.force_top_down_only = True
@@ -275,7 +280,7 @@ def workload_config(args, graph):
     kind, s, ef, offb, desc = WORKLOADS[args.workload]
     return {"workload": args.workload, "description": desc, "vertices": graph.vertex_count,
             "directed_arcs": graph.edge_count, "offset_bytes": offb, "sources": NUM_SOURCES,
-            "source_seed": SOURCE_SEED, "graph_seed": GRAPH_SEED, "variant": "hybrid",
+            "source_seed": SOURCE_SEED, "graph_seed": GRAPH_SEED, "variant": VARIANT,
             "l2": ("flushed (512 MiB memset) between launches" if args.impl == "ours"
                    else "n/a (host CPU)"),
             "parallelism": (f"{args.gpus} GPU(s)" if args.impl == "ours"
@@ -322,7 +327,12 @@ def main():
                     help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="hybrid",
+                    help="GPU kernel variant (reference names: hybrid, conventional, nonatomic, "
+                         "hybrid-beamer, visited-inline); the reference arm stays parbfs::bfs_hybrid")
     args = ap.parse_args()
+    global VARIANT
+    VARIANT = args.variant
 
     if args.impl == "reference":
         run_reference_arm(args)
