@@ -134,3 +134,23 @@ def test_large_configs_all_64_sources_bit_exact(name, port):
             want = port.bfs_serial(g.row_offsets, g.column_indices, s)
         assert np.array_equal(r.distances, want), (name, i, s)
     g.release_device()
+
+
+@pytest.mark.skipif(os.environ.get("PBFS_TEST_LARGE") != "1", reason="set PBFS_TEST_LARGE=1")
+def test_rmat26_beamer_matches_reference_beamer(port):
+    # The Beamer-rule hybrid (kernels.cpp:498-511) at full size: distances and
+    # the per-level phase / distinct-size sequence equal the reference's own
+    # parbfs::bfs_hybrid_beamer on the first 16 bench sources.
+    import oracle
+    g, offb = config_graph("rmat26")
+    dg = g.device(0, offb)
+    ref = oracle.ref()
+    rg = ref.from_csr(g.row_offsets.astype(np.uint64, copy=False), g.column_indices, True)
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.HybridBeamer)
+    for s in [int(x) for x in pb.pick_sources(g, 16, 1)]:
+        r = dg.bfs(s, cfg)
+        want, recs, _ = ref.run(rg, s, 4, workers=os.cpu_count() or 1)
+        assert np.array_equal(r.distances, want), s
+        assert [(x.depth, int(x.phase), x.distinct_size) for x in r.trace.records] == \
+            [(x["depth"], x["phase"], x["distinct_size"]) for x in recs], s
+    g.release_device()
