@@ -117,7 +117,7 @@ static_assert(kPushBuf >= 32 * PBFS_SLOTS, "a top-down batch must fit the discov
 #ifndef PBFS_BU_WIN
 #define PBFS_BU_WIN 8
 #endif
-constexpr int kBuWin = PBFS_BU_WIN;        // bottom-up scan window (8 or 16 entries)
+constexpr int kBuWin = PBFS_BU_WIN;        // bottom-up scan window (4, 8 or 16 entries)
 static_assert(kBuWin == 4 || kBuWin == 8 || kBuWin == 16, "PBFS_BU_WIN must be 4, 8 or 16");
 constexpr int kBuSlots = PBFS_BU_SLOTS;    // unvisited vertices per lane in flight
 // 32-word groups per bottom-up task: 1 (finest balance), or kBuSparseGroups
