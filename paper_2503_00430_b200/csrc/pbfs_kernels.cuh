@@ -6,37 +6,38 @@
 // between levels (the reference needs a std::barrier round and a serial
 // single-worker section per level, kernels.cpp:165-173,384-464). Per level:
 //
-//   top-down  (kernels.cpp:262-338): warps take 32-entry frontier slices
-//     (static first slice, atomic cursor only for large frontiers); vertices
-//     of degree <= kHeavyDeg are expanded warp-cooperatively (shuffle scan of
-//     degrees, kSlots edge slots per lane, owner found by a shuffle binary
-//     search); hubs are split into kChunk-edge items reserved with one
-//     atomicAdd per warp and expanded by the whole grid after a barrier, 32
-//     consecutive sorted neighbours per warp load. Every batch issues all its
-//     col loads, then all probes, then all claim atomics (predicated, no
-//     branches) before consuming any result. Claims:
+//   top-down  (kernels.cpp:262-338): warps take frontier slices of 32
+//     vertices (fewer on small frontiers; static first slice, atomic cursor
+//     only for large frontiers); vertices of degree <= kHeavyDeg are expanded
+//     warp-cooperatively (shuffle scan of degrees, PBFS_SLOTS edge slots per
+//     lane, owner found by a shuffle binary search); hubs are split into
+//     kChunk-edge items reserved with one atomicAdd per warp and expanded by
+//     the whole grid after a barrier, 32 consecutive sorted neighbours per warp
+//     load. Every batch issues all its col loads, then all probes, then all
+//     claim atomics (predicated, no branches) before consuming any result.
+//     Claims:
 //       kClaimCas    atomicCAS on dist            (BFS-Conventional)
 //       kClaimPlain  plain same-value dist stores + idempotent red.or into a
 //                    next-frontier bitmap         (BFS-NonAtomic, duplicates)
-//       kClaimBitmap visited-word probe (L1 first: bits set before the level
-//                    are reliable there and RMAT hub words stay hot; a clear
-//                    bit is re-probed at L2), atom.or claim, plain dist store,
-//                    red.or into the next-frontier bitmap (BFS-Hybrid /
-//                    VisitedBitmap)
+//       kClaimBitmap visited-word probe through L1 (a set bit is final), a
+//                    clear bit straight to atom.or, plain dist store
+//                    (BFS-Hybrid / VisitedBitmap; the partitioned engine also
+//                    red.ors winners into the next-frontier bitmap it ships)
 //     Winners go to a per-warp shared-memory buffer flushed with one
-//     atomicAdd per <= 512 entries (the GPU form of LocalFrontier +
-//     reserve_and_flush, frontier.hpp:58-98).
-//   bottom-up (kernels.cpp:340-382): warps own 16-word (512-vertex) groups of
-//     the visited bitmap and compact the unvisited ids into shared memory;
+//     atomicAdd per <= kPushBuf entries (the GPU form of LocalFrontier +
+//     reserve_and_flush, frontier.hpp:58-98). Hub-free graphs run top-down
+//     only take the latency-mode path (td_phase_latency).
+//   bottom-up (kernels.cpp:340-382): warps own 32-word (1024-vertex) groups
+//     of the visited bitmap and list the unvisited ids in shared memory;
 //     each lane probes its vertex's first neighbour (dense first_nbr array,
-//     coalesced) against the frontier bitmap and only on a miss reads rowptr
-//     and scans on in chunks of 8 until the first hit (early exit).
-//     Owner-exclusive: next/visited words are plain stores, no atomics.
+//     coalesced) against the frontier bitmap, and the misses scan on in
+//     aligned 8-entry windows with lane refill until the first hit (early
+//     exit). Owner-exclusive: next/visited words are plain stores.
 //   control (kernels.cpp:384-464,487-513): distinct size read from the level
 //     counter; `top_down = (double)distinct < thr * (double)n` evaluated in
-//     IEEE double exactly like the reference; bitmap -> queue compaction only
-//     when bottom-up hands over to top-down (top-down winners already marked
-//     the next-frontier bitmap, so the other direction needs no conversion).
+//     IEEE double exactly like the reference; bottom-up -> top-down compacts
+//     the bitmap into a queue, top-down -> bottom-up rebuilds the frontier
+//     bitmap from dist (front_from_dist).
 #pragma once
 
 #include <cooperative_groups.h>
