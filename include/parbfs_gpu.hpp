@@ -11,12 +11,14 @@
 // and rethrows C-ABI statuses as the reference exception classes
 // (types.hpp:25-68). The CsrGraph is borrowed zero-copy (its u64 offsets and
 // u32 columns are exactly pbfs_csr's layout); one device handle is cached per
-// graph identity (address, n, m, device) so a KernelFn called per source does
-// not re-upload.
+// graph identity (address, array pointers, n, m, device, content fingerprint)
+// so a KernelFn called per source does not re-upload.
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -59,19 +61,60 @@ inline pbfs_config to_c(const KernelConfig& c) {
   return out;
 }
 
-// One resident device graph per (CsrGraph address, n, m, device).
+// Resident device graphs, one per CsrGraph identity. CsrGraph is a value
+// type (csr_graph.hpp:18-29): a graph destroyed and rebuilt at the same
+// address with the same n and m (the acceptance.cpp:122 loop pattern) must not
+// reuse a stale upload. The identity is therefore (object address, the two
+// array data pointers, n, m, device) plus a content fingerprint that is
+// re-checked on every lookup (a few thousand sampled offsets and columns), and
+// the cache holds at most `capacity()` graphs (least recently used out first;
+// PARBFS_GPU_CACHE_GRAPHS overrides, default 4). Handles are shared_ptrs, so
+// an eviction never frees a graph another thread is traversing. Each entry
+// also keeps compute_stats(g), computed once per upload (the reference
+// computes it once per time_run, timing.cpp:71-77).
 class DeviceGraphCache {
  public:
+  struct Entry {
+    std::shared_ptr<pbfs_graph> graph;
+    GraphStats stats;
+  };
   static DeviceGraphCache& instance() {
     static DeviceGraphCache cache;
     return cache;
   }
-  pbfs_graph* get(const CsrGraph& g, int device) {
-    const auto key = std::make_tuple(static_cast<const void*>(&g), g.vertex_count, g.edge_count,
-                                     device);
+  static std::uint64_t fingerprint(const CsrGraph& g) {
+    std::uint64_t h = 0x9E3779B97F4A7C15ull ^ (g.symmetric ? 1u : 0u);
+    auto mix = [&h](std::uint64_t x) {
+      h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+      h *= 0xBF58476D1CE4E5B9ull;
+    };
+    const std::size_t no = g.row_offsets.size(), nc = g.column_indices.size();
+    constexpr std::size_t kSamples = 2048;
+    for (std::size_t k = 0; k < kSamples && no; ++k) mix(g.row_offsets[k * (no - 1) / (kSamples - 1)]);
+    for (std::size_t k = 0; k < kSamples && nc; ++k) {
+      mix(g.column_indices[k * (nc - 1) / (kSamples - 1)]);
+    }
+    return h;
+  }
+  std::size_t capacity() const {
+    const char* e = std::getenv("PARBFS_GPU_CACHE_GRAPHS");
+    const long v = e ? std::strtol(e, nullptr, 10) : 4;
+    return v > 0 ? static_cast<std::size_t>(v) : 1;
+  }
+  Entry get(const CsrGraph& g, int device) {
+    const Key key{static_cast<const void*>(&g), static_cast<const void*>(g.row_offsets.data()),
+                  static_cast<const void*>(g.column_indices.data()), g.vertex_count, g.edge_count,
+                  device};
+    const std::uint64_t fp = fingerprint(g);
     std::lock_guard<std::mutex> lock(mu_);
     auto it = map_.find(key);
-    if (it != map_.end()) return it->second;
+    if (it != map_.end()) {
+      if (it->second.fp == fp) {
+        it->second.last_use = ++clock_;
+        return it->second.entry;
+      }
+      map_.erase(it);  // same identity, different content: re-upload
+    }
     pbfs_csr csr{};
     csr.vertex_count = g.vertex_count;
     csr.edge_count = g.edge_count;
@@ -79,59 +122,87 @@ class DeviceGraphCache {
     csr.column_indices = g.column_indices.data();
     csr.offset_bytes = sizeof(EdgeOffset);
     csr.symmetric = g.symmetric ? 1u : 0u;
+    while (!map_.empty() && map_.size() >= capacity()) {
+      auto lru = map_.begin();
+      for (auto j = map_.begin(); j != map_.end(); ++j) {
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      }
+      map_.erase(lru);
+    }
     pbfs_graph_options opt{device, 0};
     pbfs_graph* h = nullptr;
     throw_status(pbfs_graph_create(&csr, &opt, &h));
-    map_.emplace(key, h);
-    return h;
+    Slot slot;
+    slot.entry.graph = std::shared_ptr<pbfs_graph>(h, [](pbfs_graph* x) { pbfs_graph_destroy(x); });
+    slot.entry.stats = compute_stats(g);
+    slot.fp = fp;
+    slot.last_use = ++clock_;
+    map_.emplace(key, slot);
+    return slot.entry;
   }
-  // Call when a CsrGraph is destroyed or mutated (identity is by address).
+  // Optional: drop a graph's device copy early (lookups never need it).
   void evict(const CsrGraph& g) {
     std::lock_guard<std::mutex> lock(mu_);
     for (auto it = map_.begin(); it != map_.end();) {
       if (std::get<0>(it->first) == static_cast<const void*>(&g)) {
-        pbfs_graph_destroy(it->second);
         it = map_.erase(it);
       } else {
         ++it;
       }
     }
   }
-  ~DeviceGraphCache() {
-    for (auto& kv : map_) pbfs_graph_destroy(kv.second);
+  std::size_t size() {
+    std::lock_guard<std::mutex> lock(mu_);
+    return map_.size();
   }
 
  private:
+  using Key = std::tuple<const void*, const void*, const void*, std::uint64_t, std::uint64_t, int>;
+  struct Slot {
+    Entry entry;
+    std::uint64_t fp = 0;
+    std::uint64_t last_use = 0;
+  };
   std::mutex mu_;
-  std::map<std::tuple<const void*, std::uint64_t, std::uint64_t, int>, pbfs_graph*> map_;
+  std::uint64_t clock_ = 0;
+  std::map<Key, Slot> map_;
 };
 
 // bfs_conventional / bfs_nonatomic / bfs_hybrid / bfs_hybrid_beamer /
-// bfs_visited_bitmap(inline) by config.variant, on the GPU.
-inline BfsResult bfs(const CsrGraph& g, VertexId source, const KernelConfig& config,
-                     int device = 0) {
+// bfs_visited_bitmap(inline) by config.variant, on the GPU. The trace is
+// fetched after the run, sized to the levels it actually has.
+inline BfsResult bfs_on(pbfs_graph* h, VertexId source, const KernelConfig& config,
+                        std::uint64_t vertex_count) {
   validate(config);
-  if (source >= g.vertex_count) {
+  if (source >= vertex_count) {
     throw InputError("source vertex " + std::to_string(source) +
-                     " is out of range for a graph with " + std::to_string(g.vertex_count) +
+                     " is out of range for a graph with " + std::to_string(vertex_count) +
                      " vertices");
   }
-  pbfs_graph* h = DeviceGraphCache::instance().get(g, device);
   const pbfs_config c = to_c(config);
   BfsResult r;
-  r.distances.resize(g.vertex_count);
-  std::vector<pbfs_level> levels(
-      static_cast<std::size_t>(std::min<std::uint64_t>(g.vertex_count + 1, 1u << 20)));
+  r.distances.resize(vertex_count);
   pbfs_run_info info{};
-  throw_status(pbfs_bfs(h, source, &c, r.distances.data(), levels.data(),
-                        static_cast<uint32_t>(levels.size()), &info));
+  throw_status(pbfs_bfs(h, source, &c, r.distances.data(), nullptr, 0, &info));
+  std::vector<pbfs_level> levels(info.levels);
+  std::uint32_t got = 0;
+  pbfs_status st = pbfs_graph_trace(h, levels.data(), info.levels, &got);
+  if (st == PBFS_E_CAPACITY) {
+    // Deeper than the device record buffer: one more run with a buffer for
+    // every level (the library grows its own and re-runs).
+    throw_status(pbfs_bfs(h, source, &c, r.distances.data(), levels.data(), info.levels, &info));
+    got = info.levels;
+  } else {
+    throw_status(st);
+  }
   r.trace.variant = config.variant;
   r.trace.worker_count = config.worker_count;
   r.trace.source = source;
   r.trace.same_value_violations = info.same_value_violations;
   r.trace.total_elapsed =
       std::chrono::nanoseconds(static_cast<std::int64_t>(info.device_ms * 1e6));
-  for (std::uint32_t i = 0; i < info.levels && i < levels.size(); ++i) {
+  r.trace.records.reserve(got);
+  for (std::uint32_t i = 0; i < got; ++i) {
     LevelRecord rec;
     rec.depth = levels[i].depth;
     rec.phase = levels[i].phase ? TraversalPhase::BottomUp : TraversalPhase::TopDown;
@@ -146,6 +217,13 @@ inline BfsResult bfs(const CsrGraph& g, VertexId source, const KernelConfig& con
   return r;
 }
 
+inline BfsResult bfs(const CsrGraph& g, VertexId source, const KernelConfig& config,
+                     int device = 0) {
+  validate(config);
+  const auto e = DeviceGraphCache::instance().get(g, device);
+  return bfs_on(e.graph.get(), source, config, g.vertex_count);
+}
+
 // kernels.cpp:657-691 semantics: large-diameter graphs run top-down only.
 inline BfsResult run_bfs(const CsrGraph& g, VertexId source, const KernelConfig& config,
                          const GraphStats& stats, int device = 0) {
@@ -155,9 +233,14 @@ inline BfsResult run_bfs(const CsrGraph& g, VertexId source, const KernelConfig&
 }
 
 // The plugin slot: time_run(graph, src, cfg, trials, warmups, gpu::kernel_fn()).
+// The stats come from the cached upload (computed once per graph).
 inline KernelFn kernel_fn(int device = 0) {
   return [device](const CsrGraph& g, VertexId s, const KernelConfig& c) {
-    return run_bfs(g, s, c, compute_stats(g), device);
+    validate(c);
+    const auto e = DeviceGraphCache::instance().get(g, device);
+    KernelConfig effective = c;
+    if (e.stats.category == GraphCategory::LargeDiameter) effective.force_top_down_only = true;
+    return bfs_on(e.graph.get(), s, effective, g.vertex_count);
   };
 }
 

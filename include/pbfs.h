@@ -186,6 +186,15 @@ pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cf
                            void* stream);
 pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream);
 
+/* The per-level records (parbfs::LevelRecord) of the handle's last traversal,
+ * read back after the fact, so a caller can size its buffer to the depth the
+ * run actually had (pbfs_run_info.levels) instead of to the worst case.
+ * Copies min(levels, levels_cap) records; PBFS_E_CAPACITY if the traversal
+ * was deeper than the device record buffer (pbfs_bfs with a large enough
+ * levels_cap grows it). */
+pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_cap,
+                             uint32_t* count);
+
 /* Device pointer of the distance array written by the last traversal. */
 pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev);
 

@@ -98,6 +98,7 @@ SIGNATURES = [
     ("pbfs_bfs_batch", ctypes.c_int, [c_vp, P(c_u32), c_u32, P(Config), P(c_vp), P(RunInfo)]),
     ("pbfs_bfs_async", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),
     ("pbfs_graph_sync", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_graph_trace", ctypes.c_int, [c_vp, P(Level), c_u32, P(c_u32)]),
     ("pbfs_graph_device_dist", ctypes.c_int, [c_vp, P(c_vp)]),
     ("pbfs_graph_component", ctypes.c_int, [c_vp, P(c_u64), P(c_u64)]),
     ("pbfs_host_alloc", ctypes.c_int, [ctypes.c_size_t, P(c_vp)]),

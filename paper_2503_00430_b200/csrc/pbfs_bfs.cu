@@ -197,6 +197,12 @@ struct pbfs_graph {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // Recorded right after every traversal launch on whatever stream it used;
+  // every later launch (or reset, or read of the handle's buffers) waits on
+  // it first. All traversals share the handle's ctl (grid-barrier word), bitmaps
+  // and dist, so two launches must never overlap, whichever streams the callers
+  // pass (pbfs_bfs_async) -- without holding on to a caller's stream handle.
+  cudaEvent_t order_ev = nullptr;
   uint64_t n = 0, m = 0, max_degree = 0;
   uint32_t offb = 8;
   bool symmetric = false;
@@ -284,6 +290,7 @@ void release(pbfs_graph* g) {
   if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->order_ev) cudaEventDestroy(g->order_ev);
   if (g->stream) cudaStreamDestroy(g->stream);
   cudaSetDevice(prev);
   delete g;
@@ -431,7 +438,18 @@ int occupancy_for(int claim) {
   return blocks;
 }
 
-pbfs_status prologue(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, Launch* l) {
+// Orders stream s after the handle's last launch (see pbfs_graph::order_ev).
+pbfs_status order_after_last(pbfs_graph* g, cudaStream_t s) {
+  PBFS_CUDA(cudaStreamWaitEvent(s, g->order_ev, 0), "order after the last traversal");
+  return PBFS_OK;
+}
+pbfs_status mark_launch(pbfs_graph* g, cudaStream_t s) {
+  PBFS_CUDA(cudaEventRecord(g->order_ev, s), "order event");
+  return PBFS_OK;
+}
+
+pbfs_status prologue(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, Launch* l,
+                     cudaStream_t s) {
   if (!g || !cfg) return fail(PBFS_E_INPUT, "null argument");
   pbfs_status st = pbfs_config_validate(cfg);
   if (st != PBFS_OK) return st;
@@ -450,8 +468,11 @@ pbfs_status prologue(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, Lau
                 "path");
   }
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  if ((st = order_after_last(g, s)) != PBFS_OK) return st;
   if (g->poisoned) {
-    PBFS_CUDA(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream), "reset control block");
+    // On the launching stream, after the previous launch: never under a
+    // running traversal.
+    PBFS_CUDA(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s), "reset control block");
     g->poisoned = false;
   }
   return PBFS_OK;
@@ -601,6 +622,9 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
     return bail(cuda_fail(e, "cudaStreamCreate"));
   if ((e = cudaEventCreate(&g->ev0)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
   if ((e = cudaEventCreate(&g->ev1)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  if ((e = cudaEventCreateWithFlags(&g->order_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaEventCreate"));
+  // Never recorded yet: waiting on it is a no-op until the first launch.
 
   const size_t wbytes = static_cast<size_t>(g->words) * 4;
   if ((st = dalloc(g, &g->rowptr, (n + 1) * offb)) != PBFS_OK) return bail(st);
@@ -739,12 +763,14 @@ pbfs_status pbfs_graph_get_info(const pbfs_graph* g, pbfs_graph_info* info) {
   return PBFS_OK;
 }
 
-pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uint32_t* dist_host,
-                     pbfs_level* levels, uint32_t levels_cap, pbfs_run_info* info) {
-  if (!g) return fail(PBFS_E_INPUT, "null graph");
-  std::lock_guard<std::mutex> lock(g->mu);
+}  // extern "C"
+
+namespace {
+pbfs_status pbfs_bfs_locked(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
+                            uint32_t* dist_host, pbfs_level* levels, uint32_t levels_cap,
+                            pbfs_run_info* info) {
   Launch l;
-  pbfs_status st = prologue(g, source, cfg, &l);
+  pbfs_status st = prologue(g, source, cfg, &l, g->stream);
   if (st != PBFS_OK) return st;
   cudaError_t e;
   PBFS_CUDA(cudaEventRecord(g->ev0, g->stream), "event record");
@@ -753,6 +779,7 @@ pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uin
     return cuda_fail(e, "traversal launch");
   }
   PBFS_CUDA(cudaEventRecord(g->ev1, g->stream), "event record");
+  if ((st = mark_launch(g, g->stream)) != PBFS_OK) return st;
   Ctl ctl;
   PBFS_CUDA(cudaMemcpyAsync(&ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream), "read control");
   if ((e = cudaStreamSynchronize(g->stream)) != cudaSuccess) {
@@ -782,10 +809,34 @@ pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uin
     cudaEventElapsedTime(&ms, g->ev0, g->ev1);
     info->device_ms = ms;
   }
-  if (ctl.levels > g->rec_cap && levels) {
-    return fail(PBFS_E_CAPACITY, "traversal depth exceeds the device trace capacity");
+  if (ctl.levels > g->rec_cap && levels && levels_cap > g->rec_cap) {
+    // Deeper than the device record buffer (min(n + 1, 2^20) levels): grow it
+    // to the depth just seen and run the traversal again, so any depth is
+    // recorded (the reference records every level, trace.hpp:37-48).
+    pbfs_level* bigger = nullptr;
+    PBFS_CUDA(cudaMalloc(&bigger, static_cast<size_t>(ctl.levels) * sizeof(pbfs_level)),
+              "grow the trace buffer");
+    for (auto& a : g->allocs) {
+      if (a == g->records) a = bigger;
+    }
+    cudaFree(g->records);
+    g->device_bytes += static_cast<uint64_t>(ctl.levels - g->rec_cap) * sizeof(pbfs_level);
+    g->records = bigger;
+    g->rec_cap = ctl.levels;
+    return pbfs_bfs_locked(g, source, cfg, dist_host, levels, levels_cap, info);
   }
   return PBFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uint32_t* dist_host,
+                     pbfs_level* levels, uint32_t levels_cap, pbfs_run_info* info) {
+  if (!g) return fail(PBFS_E_INPUT, "null graph");
+  std::lock_guard<std::mutex> lock(g->mu);
+  return pbfs_bfs_locked(g, source, cfg, dist_host, levels, levels_cap, info);
 }
 
 pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t count,
@@ -796,7 +847,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   std::lock_guard<std::mutex> lock(g->mu);
   Launch l;
   for (uint32_t i = 0; i < count; ++i) {
-    pbfs_status st = prologue(g, sources[i], cfg, &l);
+    pbfs_status st = prologue(g, sources[i], cfg, &l, g->stream);
     if (st != PBFS_OK) return st;
   }
   if (count == 0) return PBFS_OK;
@@ -916,6 +967,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     }
     if (i >= 1 && (e = finish(i - 1)) != cudaSuccess) break;
   }
+  if (e == cudaSuccess) e = cudaEventRecord(g->order_ev, g->stream);
   cudaError_t e1 = cudaStreamSynchronize(g->stream);
   cudaError_t e2 = cudaStreamSynchronize(g->copy_stream);
   // Every callback that fired has submitted its job; wait for those.
@@ -955,15 +1007,15 @@ pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cf
   if (!g) return fail(PBFS_E_INPUT, "null graph");
   std::lock_guard<std::mutex> lock(g->mu);
   Launch l;
-  pbfs_status st = prologue(g, source, cfg, &l);
-  if (st != PBFS_OK) return st;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
+  pbfs_status st = prologue(g, source, cfg, &l, s);
+  if (st != PBFS_OK) return st;
   cudaError_t e = launch(g, source, cfg, l, s);
   if (e != cudaSuccess) {
     g->poisoned = true;
     return cuda_fail(e, "traversal launch");
   }
-  return PBFS_OK;
+  return mark_launch(g, s);
 }
 
 pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream) {
@@ -972,6 +1024,8 @@ pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream) {
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
   cudaError_t e = cudaStreamSynchronize(s);
+  // Also the handle's last traversal, if it went to another stream.
+  if (e == cudaSuccess) e = cudaEventSynchronize(g->order_ev);
   if (e != cudaSuccess) {
     g->poisoned = true;
     return cuda_fail(e, "traversal");
@@ -997,6 +1051,26 @@ pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offse
   return PBFS_OK;
 }
 
+pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_cap,
+                             uint32_t* count) {
+  if (!g || !count || (levels_cap && !levels)) return fail(PBFS_E_INPUT, "null argument");
+  std::lock_guard<std::mutex> lock(g->mu);
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PBFS_CUDA(cudaEventSynchronize(g->order_ev), "traversal");
+  unsigned int nlev = 0;
+  PBFS_CUDA(cudaMemcpy(&nlev, &g->ctl->levels, sizeof(nlev), cudaMemcpyDeviceToHost), "read control");
+  const uint32_t k = std::min<uint32_t>(std::min<uint32_t>(nlev, g->rec_cap), levels_cap);
+  if (k) {
+    PBFS_CUDA(cudaMemcpy(levels, g->records, k * sizeof(pbfs_level), cudaMemcpyDeviceToHost),
+              "read trace");
+  }
+  *count = k;
+  if (nlev > g->rec_cap) {
+    return fail(PBFS_E_CAPACITY, "the last traversal was deeper than the device trace buffer");
+  }
+  return PBFS_OK;
+}
+
 pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev) {
   if (!g || !dist_dev) return fail(PBFS_E_INPUT, "null argument");
   *dist_dev = g->dist;
@@ -1007,6 +1081,8 @@ pbfs_status pbfs_graph_component(pbfs_graph* g, uint64_t* n_reached, uint64_t* a
   if (!g || !n_reached || !arcs_reached) return fail(PBFS_E_INPUT, "null argument");
   std::lock_guard<std::mutex> lock(g->mu);
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  pbfs_status st = order_after_last(g, g->stream);
+  if (st != PBFS_OK) return st;
   PBFS_CUDA(cudaMemsetAsync(g->comp, 0, 2 * sizeof(unsigned long long), g->stream), "memset");
   if (g->offb == 8) {
     component_kernel<unsigned long long><<<g->grid, kThreads, 0, g->stream>>>(

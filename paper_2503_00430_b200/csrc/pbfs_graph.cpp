@@ -429,9 +429,17 @@ pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads) {
     return fail(PBFS_E_FORMAT, "offset array ends at " + std::to_string(csr_offset(c, c->vertex_count)) +
                                    " but edge count is " + std::to_string(c->edge_count));
   }
-  const uint64_t n = c->vertex_count;
+  const uint64_t n = c->vertex_count, m = c->edge_count;
   threads = std::max(1u, std::min<unsigned>(threads, n / 65536 + 1));
   std::vector<std::string> errs(threads);
+  auto first_error = [&]() -> pbfs_status {
+    for (auto& e : errs) {
+      if (!e.empty()) return fail(PBFS_E_FORMAT, e);
+    }
+    return PBFS_OK;
+  };
+  // Pass 1: every offset is non-decreasing and <= m before any column is
+  // read (a crafted offset must not send pass 2 outside column_indices).
   parallel_for_threads(threads, [&](unsigned t) {
     const uint64_t b = n * t / threads, e = n * (t + 1) / threads;
     for (uint64_t v = b; v < e; ++v) {
@@ -440,6 +448,19 @@ pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads) {
         errs[t] = "offset array decreases at vertex " + std::to_string(v);
         return;
       }
+      if (hi > m) {
+        errs[t] = "offset of vertex " + std::to_string(v + 1) + " exceeds the edge count";
+        return;
+      }
+    }
+  });
+  pbfs_status st = first_error();
+  if (st != PBFS_OK) return st;
+  // Pass 2: neighbour ids in range and strictly increasing per row.
+  parallel_for_threads(threads, [&](unsigned t) {
+    const uint64_t b = n * t / threads, e = n * (t + 1) / threads;
+    for (uint64_t v = b; v < e; ++v) {
+      const uint64_t lo = csr_offset(c, v), hi = csr_offset(c, v + 1);
       for (uint64_t k = lo; k < hi; ++k) {
         const uint32_t x = c->column_indices[k];
         if (x >= n) {
@@ -454,10 +475,7 @@ pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads) {
       }
     }
   });
-  for (auto& e : errs) {
-    if (!e.empty()) return fail(PBFS_E_FORMAT, e);
-  }
-  return PBFS_OK;
+  return first_error();
 }
 
 }  // namespace pbfs
@@ -625,7 +643,31 @@ pbfs_status pbfs_load_csr1(const char* path, pbfs_host_csr** out) {
     std::fclose(f);
     return fail(PBFS_E_FORMAT, name + ": vertex count exceeds the supported maximum");
   }
+  // The header's counts must describe exactly the bytes that follow it
+  // (graph_io.cpp:100-116 rejects short and trailing data): checked before
+  // any allocation, so a crafted m cannot wrap m * 4 or over-allocate.
+  const long long here = ftello(f);
+  long long end = -1;
+  if (here >= 0 && fseeko(f, 0, SEEK_END) == 0) end = ftello(f);
+  if (end < 0 || fseeko(f, here, SEEK_SET) != 0) {
+    std::fclose(f);
+    return fail(PBFS_E_FORMAT, name + ": cannot determine the file size");
+  }
+  const uint64_t body = static_cast<uint64_t>(end - here);
+  const uint64_t off_bytes = (n + 1) * 8;
+  if (body < off_bytes) {
+    std::fclose(f);
+    return fail(PBFS_E_FORMAT, name + ": truncated graph data");
+  }
+  if (m > (body - off_bytes) / 4) {
+    std::fclose(f);
+    return fail(PBFS_E_FORMAT, name + ": truncated graph data");
+  }
   auto* h = new (std::nothrow) pbfs_host_csr;
+  if (!h) {
+    std::fclose(f);
+    return fail(PBFS_E_CAPACITY, name + ": host allocation failed");
+  }
   h->g.n = n;
   h->g.m = m;
   h->g.offsets.reset(new (std::nothrow) uint64_t[n + 1]);

@@ -687,7 +687,12 @@ pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void*
   while ((1ull << k) < g->n) ++k;
   const bool pow2 = (1ull << k) == g->n;
   const uint64_t quantum = 512ull * g->world;
-  if (pow2 && opt->relabel && g->n >= quantum) {
+  // The hashed bijection lives on [0, 2^k): its equal ownership ranges
+  // [r * n / world, ...) tile it exactly only when world divides 2^k into
+  // whole 512-vertex groups, i.e. world is a power of two and n >= quantum.
+  // Any other world size (3, 5, 6, 7) takes identity + padding.
+  const bool world_pow2 = (g->world & (g->world - 1)) == 0;
+  if (pow2 && world_pow2 && opt->relabel && g->n >= quantum) {
     g->npad = g->n;
     g->rl = make_relabel(k, true);
   } else {

@@ -538,6 +538,14 @@ class DeviceGraph:
         _check(lib.pbfs_bfs(self.h, int(source) & 0xFFFFFFFF, ctypes.byref(c),
                             dist.ctypes.data if dist is not None else None, levels, cap,
                             ctypes.byref(info)))
+        if cap and info.levels > cap:
+            # Deeper than the default record buffer: ask again for every level
+            # (the library grows its device trace buffer and re-runs).
+            cap = int(info.levels)
+            levels = (L.Level * cap)()
+            _check(lib.pbfs_bfs(self.h, int(source) & 0xFFFFFFFF, ctypes.byref(c),
+                                dist.ctypes.data if dist is not None else None, levels, cap,
+                                ctypes.byref(info)))
         t1 = time.perf_counter_ns()
         trace = TraversalTrace(variant=KernelVariant(config.variant),
                                worker_count=config.worker_count, source=int(source),

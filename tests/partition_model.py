@@ -24,7 +24,8 @@ class Relabel:
     def __init__(self, n, world, hashed=True):
         k = max(1, (n - 1).bit_length())
         quantum = 512 * world
-        if (1 << k) == n and hashed and n >= quantum and k >= 2:
+        world_pow2 = world & (world - 1) == 0
+        if (1 << k) == n and world_pow2 and hashed and n >= quantum and k >= 2:
             self.hashed, self.npad = True, n
         else:
             self.hashed, self.npad = False, (n + quantum - 1) // quantum * quantum

@@ -397,3 +397,49 @@ def test_latency_mode_matches_the_general_top_down(offset_bytes, port, monkeypat
             g.release_device()
         for s in srcs:
             assert recs["1", s] == recs["0", s]
+
+
+def test_async_on_two_streams_is_ordered(port):
+    # pbfs_bfs_async on caller streams: every launch waits for the handle's
+    # previous one (they share ctl / bitmaps / dist), whichever streams the
+    # callers pass; then pbfs_bfs on the handle's own stream and the
+    # component read see the last traversal.
+    import torch
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 16, 16, 2,
+                                     drop_self_loops=True))
+    dg = g.device(0, 8)
+    srcs = [int(s) for s in pb.pick_sources(g, 6, 3)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    cfg = pb.KernelConfig(variant=V.Hybrid)
+    for i, s in enumerate(srcs):
+        dg.bfs_async(s, cfg, streams[i % 2].cuda_stream)
+    # No host sync in between: the component read must follow the last launch.
+    nr, ar = dg.component()
+    want = port.bfs_serial(g.row_offsets, g.column_indices, srcs[-1])
+    assert (nr, ar) == port.component(g.row_offsets, want)
+    for i, s in enumerate(srcs):
+        dg.bfs_async(s, cfg, streams[i % 2].cuda_stream)
+        got = dg.bfs(srcs[0], cfg).distances
+        assert np.array_equal(got, port.bfs_serial(g.row_offsets, g.column_indices, srcs[0]))
+    dg.sync(streams[0].cuda_stream)
+
+
+def test_trace_deeper_than_the_default_record_buffer(port):
+    # A path of 2^20 + 40 vertices: more levels than the default device record
+    # buffer (2^20); every level is still recorded (trace.hpp:37-48).
+    n = (1 << 20) + 40
+    off = np.zeros(n + 1, dtype=np.uint64)
+    deg = np.full(n, 2, dtype=np.uint64)
+    deg[0] = deg[-1] = 1
+    off[1:] = np.cumsum(deg)
+    col = np.empty(int(off[-1]), dtype=np.uint32)
+    v = np.arange(n, dtype=np.int64)
+    left = off[:-1].astype(np.int64)
+    col[left[1:]] = v[1:] - 1                      # left neighbour first (ascending)
+    col[left[:-1] + (v[:-1] > 0)] = v[:-1] + 1     # then the right one
+    g = pb.CsrGraph(n, off, col, True)
+    cfg = pb.KernelConfig(variant=V.Hybrid, force_top_down_only=True)
+    r = g.device(0, 8).bfs(0, cfg)
+    assert np.array_equal(r.distances, np.arange(n, dtype=np.uint32))
+    assert len(r.trace.records) == n
+    assert r.trace.records[-1].depth == n - 1 and r.trace.records[-1].distinct_size == 1

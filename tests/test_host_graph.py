@@ -157,6 +157,19 @@ def test_csr1_roundtrip_and_errors(tmp_path):
         pb.load_binary_csr(str(bad))
     with pytest.raises(pb.InputError):
         pb.load_binary_csr(str(tmp_path / "missing.csr"))
+    # A crafted edge count (m * 4 wraps 64 bits) is rejected from the file
+    # size before any allocation.
+    bad.write_bytes(raw[:12] + ((1 << 62) + 1).to_bytes(8, "little") + raw[20:])
+    with pytest.raises(pb.FormatError, match="truncated"):
+        pb.load_binary_csr(str(bad))
+    # A huge interior offset is caught by the offsets-first pass, before any
+    # column read.
+    n = g.vertex_count
+    offs = bytearray(raw[20:20 + 8 * (n + 1)])
+    offs[8 * 5:8 * 6] = (1 << 40).to_bytes(8, "little")
+    bad.write_bytes(raw[:20] + bytes(offs) + raw[20 + 8 * (n + 1):])
+    with pytest.raises(pb.FormatError, match="decreases|exceeds"):
+        pb.load_binary_csr(str(bad))
 
 
 def test_validate_csr_errors():

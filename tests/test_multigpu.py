@@ -83,7 +83,7 @@ def test_partition_protocol_gloo(world):
 
 
 def test_relabel_is_a_bijection():
-    for n, world in [(1 << 14, 2), (1 << 16, 8), (5000, 4)]:
+    for n, world in [(1 << 14, 2), (1 << 16, 8), (5000, 4), (1 << 14, 3), (1 << 16, 6)]:
         rl = pm.Relabel(n, world)
         img = rl.fwd(np.arange(n, dtype=np.uint64))
         assert len(np.unique(img)) == n and int(img.max()) < rl.npad
@@ -131,7 +131,7 @@ def test_loopback_identity_relabel_and_padding(port):
 
 
 def test_gid_map_is_order_preserving_and_balanced():
-    for n, world in [(1 << 14, 2), (1 << 16, 8), (5000, 4)]:
+    for n, world in [(1 << 14, 2), (1 << 16, 8), (5000, 4), (1 << 14, 3), (1 << 14, 7)]:
         rl, nloc, gid = pm.gid_map(n, world)
         assert len(np.unique(gid)) == n and int(gid.max()) < rl.npad
         owner = gid // nloc
@@ -140,6 +140,25 @@ def test_gid_map_is_order_preserving_and_balanced():
             assert (np.diff(gid[mine]) == 1).all()   # consecutive, same order
         if rl.hashed:
             assert (np.bincount(owner, minlength=world) == nloc).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [3, 6])
+def test_loopback_non_power_of_two_world_on_kronecker(world, port):
+    # n = 2^14 is a power of two but world is not: the partition must fall
+    # back to identity + padding (the hashed ranges would not tile 2^k).
+    import paper_2503_00430_b200 as pb
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 14, 16, 1,
+                                     drop_self_loops=True))
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid)
+    parts = None
+    for s in pb.pick_sources(g, 3, 1):
+        want = port.bfs_serial(g.row_offsets, g.column_indices, int(s))
+        got, _, parts = pb.bfs_partitioned_loopback(g, int(s), cfg, world, parts=parts)
+        assert np.array_equal(got, want), (world, int(s))
+    info = parts[0].info()
+    assert info["relabel_hashed"] == 0 and info["padded_count"] % (512 * world) == 0
+    assert sum(p.info()["local_arcs"] for p in parts) == g.edge_count
 
 
 @pytest.mark.gpu
