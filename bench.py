@@ -180,10 +180,12 @@ def harmonic(values):
     return len(values) / sum(1.0 / v for v in values) if values else 0.0
 
 
-def cpu_reference_run(graph, sources, cfg, budget_s: float, e_r: dict, check_dist=None):
+def cpu_reference_run(graph, sources, cfg, budget_s: float, e_r: dict, gpu_dist=None):
     """The reference's own hybrid BFS (oracle/_ref, all host threads) on the
-    same CSR and sources; returns (per-source GTEPS list, sample text, cores,
-    kind, mismatches)."""
+    same CSR and sources, for about `budget_s` seconds; every source it runs
+    is also checked bit-exactly against the GPU's distances (gpu_dist(s)).
+    Returns (per-source GTEPS list, sample text, cores, kind, checked,
+    mismatches)."""
     import oracle
     threads = os.cpu_count() or 1
     kind = "reference"
@@ -192,99 +194,156 @@ def cpu_reference_run(graph, sources, cfg, budget_s: float, e_r: dict, check_dis
     except Exception as exc:  # the reference library did not travel: port
         log(f"[bench] reference library unavailable ({exc}); timing the oracle port")
         ref = None
-    gteps, done, mismatches = [], 0, 0
+    gteps, done, checked, mismatches = [], 0, 0, 0
     t_start = time.time()
-    if ref is not None:
-        rg = ref.from_csr(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
-                          graph.symmetric)
-        for s in sources:
+    off64 = graph.row_offsets.astype(np.uint64, copy=False)
+    rg = ref.from_csr(off64, graph.column_indices, graph.symmetric) if ref is not None else None
+    port = oracle.port() if ref is None else None
+    for s in sources:
+        if ref is not None:
             dist, _, wall_ns = ref.run(rg, int(s), 3, workers=threads,
-                                       force_td=cfg.force_top_down_only,
-                                       want_dist=check_dist is not None)
-            if check_dist is not None and int(s) in check_dist:
-                mismatches += int(not np.array_equal(dist, check_dist[int(s)]))
-            gteps.append(e_r[int(s)] / (wall_ns * 1e-9) / 1e9)
-            done += 1
-            if time.time() - t_start > budget_s:
-                break
+                                       force_td=cfg.force_top_down_only, want_dist=True)
+            t = wall_ns * 1e-9
+        else:
+            t0 = time.perf_counter_ns()
+            dist = port.bfs_serial(off64, graph.column_indices, int(s))
+            t = (time.perf_counter_ns() - t0) * 1e-9
+        if gpu_dist is not None:
+            checked += 1
+            mismatches += int(not np.array_equal(dist, gpu_dist(int(s))))
+        gteps.append(e_r[int(s)] / t / 1e9)
+        done += 1
+        if time.time() - t_start > budget_s:
+            break
+    if ref is not None:
         sample = (f"{done} of {len(sources)} sources, 1 run each, parbfs::bfs_hybrid "
                   f"(threshold 0.05{', force_top_down_only' if cfg.force_top_down_only else ''}) "
                   f"with worker_count={threads}, steady-clock wall per call incl. its setup")
     else:
         kind, threads = "port", 1
-        port = oracle.port()
-        for s in sources:
-            t0 = time.perf_counter_ns()
-            port.bfs_serial(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
-                            int(s))
-            gteps.append(e_r[int(s)] / ((time.perf_counter_ns() - t0) * 1e-9) / 1e9)
-            done += 1
-            if time.time() - t_start > budget_s:
-                break
         sample = f"{done} of {len(sources)} sources, oracle serial BFS, 1 thread"
-    return gteps, sample, threads, kind, mismatches
+    return gteps, sample, threads, kind, checked, mismatches
+
+
+def build_graph_oracle(name: str):
+    """The reference arm's graph, built by the test oracle alone (oracle/:
+    the C restatement of generator.cpp / csr_graph.cpp, pinned bit-exact to
+    the reference's own generate() by tests/test_oracle.py), so that the
+    reference arm never loads the product library."""
+    import oracle
+    port = oracle.port()
+    kind, s, ef, _, _ = WORKLOADS[name]
+    t0 = time.time()
+    if kind == "mesh":
+        pairs, n = port.mesh_pairs(s, seed=GRAPH_SEED), s * s
+    else:
+        pairs, n = port.generate_pairs(1 if kind == "kron" else 0, s, ef, GRAPH_SEED), 1 << s
+    off, col = port.build_csr(pairs, n, symmetrize=True, drop_self_loops=True)
+    del pairs
+    log(f"[bench] oracle-built {name}: n={n} m={col.size} in {time.time()-t0:.1f}s")
+    return off, col
 
 
 def run_reference_arm(args):
-    """bench.py --impl reference: rank 0 only, the reference CPU BFS."""
+    """bench.py --impl reference: rank 0 only, the reference's own hybrid BFS
+    (parbfs::bfs_hybrid from oracle/_ref, all host threads) on the same CSR,
+    sources and config as the GPU arm. The graph comes from the oracle port,
+    so this process never loads libpbfs.so. The K timed steps together cover
+    all 64 sources: step i runs the next ceil(64 / K) of them (cyclically),
+    and the value is the harmonic mean over the 64 per-source GTEPS."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2503_00430_b200 as pb
-    graph = build_graph(args.workload)
-    cfg, _ = kernel_config(graph)
-    sources = pb.pick_sources(graph, NUM_SOURCES, SOURCE_SEED)
-    deg = graph.degrees()
-    # E_r per source from the reference's own serial traversal would cost
-    # minutes at scale 26; the reference hybrid returns distances, so E_r is
-    # taken from each run's reached set.
     import oracle
-    ref = oracle.ref()
-    rg = ref.from_csr(graph.row_offsets.astype(np.uint64, copy=False), graph.column_indices,
-                      graph.symmetric)
+    port = oracle.port()
+    off, col = build_graph_oracle(args.workload)
+    n = off.size - 1
+    deg = np.diff(off).astype(np.int64)
+    avg, _, large = port.stats(off)
+    force_td = bool(large)  # run_bfs's dispatcher (kernels.cpp:657-662)
     threads = os.cpu_count() or 1
-    per_step = []
-    all_gteps = []
-    budget = args.ref_step_budget
-    for step in range(args.warmup + args.steps):
-        t_step = time.time()
-        g_list = []
-        for s in sources:
-            dist, _, wall_ns = ref.run(rg, int(s), 3, workers=threads,
-                                       force_td=cfg.force_top_down_only)
-            e_r = float(deg[dist != 0xFFFFFFFF].sum()) / 2.0
-            g_list.append(e_r / (wall_ns * 1e-9) / 1e9)
-            if time.time() - t_step > budget:
+    try:
+        ref = oracle.ref()
+        rg = ref.from_csr(off, col, True)
+    except Exception as exc:  # the reference library did not travel: time the port
+        log(f"[bench] reference library unavailable ({exc}); timing the oracle port")
+        ref = rg = None
+    sources = [int(v) for v in port.pick_sources(off, NUM_SOURCES, SOURCE_SEED)]
+    if args.workload == "mesh4096":
+        # Same rule as the GPU arm's choose_sources: candidates inside the
+        # largest component (found with one traversal).
+        cand = [int(v) for v in port.pick_sources(off, 4 * NUM_SOURCES, SOURCE_SEED)]
+        for c in cand:
+            d = port.bfs_serial(off, col, c)
+            reached = d != 0xFFFFFFFF
+            if reached.sum() * 2 > n:
+                sources = [v for v in cand if reached[v]][:NUM_SOURCES]
                 break
-        if step >= args.warmup:
-            per_step.append(time.time() - t_step)
-            all_gteps.extend(g_list)
-    value = harmonic(all_gteps)
-    sample = (f"{len(all_gteps)} source runs over {args.steps} steps (each step <= "
-              f"{budget:.0f}s of the 64 sources), parbfs::bfs_hybrid worker_count={threads}")
+
+    def one(src):
+        if ref is not None:
+            dist, _, wall_ns = ref.run(rg, src, 3, workers=threads, force_td=force_td)
+            t = wall_ns * 1e-9
+        else:
+            t0 = time.perf_counter()
+            dist = port.bfs_serial(off, col, src)
+            t = time.perf_counter() - t0
+        e_r = float(deg[dist != 0xFFFFFFFF].sum()) / 2.0
+        return e_r / t / 1e9
+
+    per_step = -(-len(sources) // max(1, args.steps))
+    cursor = 0
+    for _ in range(args.warmup):  # one untimed source per warm-up step
+        one(sources[cursor % len(sources)])
+        cursor += 1
+    cursor = 0
+    per_src = {}
+    step_s = []
+    for _ in range(args.steps):
+        t_step = time.time()
+        for _ in range(per_step):
+            src = sources[cursor % len(sources)]
+            per_src.setdefault(src, []).append(one(src))
+            cursor += 1
+        step_s.append(time.time() - t_step)
+    # each source once in the harmonic mean (its median if it ran twice)
+    value = harmonic([statistics.median(v) for v in per_src.values()])
+    covered = len(per_src)
+    impl = "parbfs::bfs_hybrid worker_count=%d" % threads if ref is not None else \
+        "oracle serial BFS, 1 thread"
+    sample = (f"{covered} of {len(sources)} sources ({per_step} per timed step over {args.steps} "
+              f"steps, cyclic), {impl}, steady-clock wall per call incl. its per-run setup; "
+              f"graph built by the oracle port (no product library in this process)")
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GTEPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * statistics.mean(per_step), 3) if per_step else None,
+        "ms_per_step": round(1e3 * statistics.mean(step_s), 3) if step_s else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": workload_config(args, graph),
-        "cpu_baseline": {"value": round(value, 4), "unit": "GTEPS", "cores": threads,
-                         "kind": "reference", "sample": sample},
+        "data": "synthetic",
+        "config": {**workload_config_raw(args, n, int(col.size)),
+                   "sources_covered": covered, "same_config": covered == len(sources)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GTEPS",
+                         "cores": threads if ref is not None else 1,
+                         "kind": "reference" if ref is not None else "port", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
-def workload_config(args, graph):
+def workload_config_raw(args, n, m):
     kind, s, ef, offb, desc = WORKLOADS[args.workload]
-    return {"workload": args.workload, "description": desc, "vertices": graph.vertex_count,
-            "directed_arcs": graph.edge_count, "offset_bytes": offb, "sources": NUM_SOURCES,
+    return {"workload": args.workload, "description": desc, "vertices": n,
+            "directed_arcs": m, "offset_bytes": offb, "sources": NUM_SOURCES,
             "source_seed": SOURCE_SEED, "graph_seed": GRAPH_SEED, "variant": VARIANT,
             "l2": ("flushed (512 MiB memset) between launches" if args.impl == "ours"
                    else "n/a (host CPU)"),
             "parallelism": (f"{args.gpus} GPU(s)" if args.impl == "ours"
                             else f"reference std::thread workers on {os.cpu_count()} host cores")}
+
+
+def workload_config(args, graph):
+    return workload_config_raw(args, graph.vertex_count, graph.edge_count)
 
 
 class _DeviceArray:
@@ -325,7 +384,6 @@ def main():
                          "partitions)")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work for cpu_baseline")
-    ap.add_argument("--ref-step-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="hybrid",
                     help="GPU kernel variant (reference names: hybrid, conventional, nonatomic, "
@@ -458,13 +516,12 @@ def run_single(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        check = {}
-        for s in sources[:2]:
-            check[s] = dg.bfs(s, cfg, want_trace=False).distances.copy()
-        cg, sample, cores, kind, mism = cpu_reference_run(graph, sources, cfg, args.cpu_budget,
-                                                          e_r, check)
+        def gpu_dist(s):
+            return dg.bfs(s, cfg, want_trace=False).distances.copy()
+        cg, sample, cores, kind, checked, mism = cpu_reference_run(
+            graph, sources, cfg, args.cpu_budget, e_r, gpu_dist)
         cpu = {"value": round(harmonic(cg), 4), "unit": "GTEPS", "cores": cores, "kind": kind,
-               "sample": sample, "parity_checked_sources": len(check),
+               "sample": sample, "parity_checked_sources": checked,
                "parity_mismatches": mism}
 
     out = {

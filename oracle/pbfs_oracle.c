@@ -20,16 +20,29 @@ void orc_mt64_seed(orc_mt64* s, uint64_t seed) {
   s->idx = MT_N;
 }
 
-uint64_t orc_mt64_next(orc_mt64* s) {
-  if (s->idx >= MT_N) {
-    for (uint32_t i = 0; i < MT_N; ++i) {
-      uint64_t x = (s->mt[i] & MT_UPPER) | (s->mt[(i + 1) % MT_N] & MT_LOWER);
-      uint64_t xa = x >> 1;
-      if (x & 1) xa ^= MT_A;
-      s->mt[i] = s->mt[(i + MT_M) % MT_N] ^ xa;
-    }
-    s->idx = 0;
+/* The twist of all 312 words, written as its three index ranges so no
+ * modulo sits in the loop (same recurrence as the textbook form
+ * x[i] = x[(i+m) % n] ^ A(upper(x[i]) | lower(x[(i+1) % n]))). */
+static void mt64_twist(orc_mt64* s) {
+  uint64_t* x = s->mt;
+  uint32_t i = 0;
+  for (; i < MT_N - MT_M; ++i) {
+    const uint64_t y = (x[i] & MT_UPPER) | (x[i + 1] & MT_LOWER);
+    x[i] = x[i + MT_M] ^ (y >> 1) ^ ((y & 1) ? MT_A : 0);
   }
+  for (; i < MT_N - 1; ++i) {
+    const uint64_t y = (x[i] & MT_UPPER) | (x[i + 1] & MT_LOWER);
+    x[i] = x[i + MT_M - MT_N] ^ (y >> 1) ^ ((y & 1) ? MT_A : 0);
+  }
+  {
+    const uint64_t y = (x[MT_N - 1] & MT_UPPER) | (x[0] & MT_LOWER);
+    x[MT_N - 1] = x[MT_M - 1] ^ (y >> 1) ^ ((y & 1) ? MT_A : 0);
+  }
+  s->idx = 0;
+}
+
+static inline uint64_t mt64_next(orc_mt64* s) {
+  if (s->idx >= MT_N) mt64_twist(s);
   uint64_t y = s->mt[s->idx++];
   y ^= (y >> 29) & 0x5555555555555555ULL;
   y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
@@ -38,12 +51,14 @@ uint64_t orc_mt64_next(orc_mt64* s) {
   return y;
 }
 
+uint64_t orc_mt64_next(orc_mt64* s) { return mt64_next(s); }
+
 /* Sampler::bounded / Sampler::unit — generator.cpp:22-29 */
-static uint64_t bounded(orc_mt64* s, uint64_t n) {
-  return (uint64_t)(((unsigned __int128)orc_mt64_next(s) * n) >> 64);
+static inline uint64_t bounded(orc_mt64* s, uint64_t n) {
+  return (uint64_t)(((unsigned __int128)mt64_next(s) * n) >> 64);
 }
-static double unit(orc_mt64* s) {
-  return (double)(orc_mt64_next(s) >> 11) * 0x1.0p-53;
+static inline double unit(orc_mt64* s) {
+  return (double)(mt64_next(s) >> 11) * 0x1.0p-53;
 }
 
 /* generator.cpp:41-89 */
@@ -60,19 +75,16 @@ int orc_generate_pairs(int kind, uint32_t scale, uint32_t edge_factor,
       row = bounded(&s, n);
       col = bounded(&s, n);
     } else {
+      /* generator.cpp:75-84's quadrant chain r < a | < a+b | < a+b+c | else,
+       * as comparisons (same double thresholds, no branches):
+       * row bit set for quadrants c and d, column bit for b and d. */
+      const double ta = 0.57, tab = 0.57 + 0.19, tabc = 0.57 + 0.19 + 0.19;
       for (uint32_t l = 0; l < scale; ++l) {
         const double r = unit(&s);
-        row <<= 1;
-        col <<= 1;
-        if (r < 0.57) {
-        } else if (r < 0.57 + 0.19) {
-          col |= 1;
-        } else if (r < 0.57 + 0.19 + 0.19) {
-          row |= 1;
-        } else {
-          row |= 1;
-          col |= 1;
-        }
+        const uint64_t rb = r >= tab;
+        const uint64_t cb = ((uint64_t)(r >= ta) & (uint64_t)(r < tab)) | (uint64_t)(r >= tabc);
+        row = (row << 1) | rb;
+        col = (col << 1) | cb;
       }
     }
     pairs[2 * i] = (uint32_t)row;
@@ -81,58 +93,84 @@ int orc_generate_pairs(int kind, uint32_t scale, uint32_t edge_factor,
   return 0;
 }
 
-/* LSD radix sort of 64-bit keys, 16-bit digits. */
-static void radix_sort_u64(uint64_t* a, uint64_t* tmp, uint64_t len) {
-  uint64_t* src = a;
-  uint64_t* dst = tmp;
-  uint64_t* count = (uint64_t*)malloc(sizeof(uint64_t) * 65536);
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 16 * pass;
-    memset(count, 0, sizeof(uint64_t) * 65536);
-    for (uint64_t i = 0; i < len; ++i) count[(src[i] >> shift) & 0xFFFF]++;
+/* Ascending sort of a row: insertion sort for short rows, else an LSD radix
+ * sort (four 8-bit digits) through `tmp` (len entries). */
+static void sort_u32(uint32_t* a, uint64_t len, uint32_t* tmp) {
+  if (len <= 32) {
+    for (uint64_t i = 1; i < len; ++i) {
+      const uint32_t x = a[i];
+      uint64_t j = i;
+      while (j > 0 && a[j - 1] > x) {
+        a[j] = a[j - 1];
+        --j;
+      }
+      a[j] = x;
+    }
+    return;
+  }
+  uint64_t count[256];
+  uint32_t* src = a;
+  uint32_t* dst = tmp;
+  for (int shift = 0; shift < 32; shift += 8) {
+    memset(count, 0, sizeof(count));
+    for (uint64_t i = 0; i < len; ++i) count[(src[i] >> shift) & 0xFF]++;
     uint64_t sum = 0;
-    for (int d = 0; d < 65536; ++d) {
-      uint64_t c = count[d];
+    for (int d = 0; d < 256; ++d) {
+      const uint64_t c = count[d];
       count[d] = sum;
       sum += c;
     }
-    for (uint64_t i = 0; i < len; ++i) dst[count[(src[i] >> shift) & 0xFFFF]++] = src[i];
-    uint64_t* t = src;
+    for (uint64_t i = 0; i < len; ++i) dst[count[(src[i] >> shift) & 0xFF]++] = src[i];
+    uint32_t* t = src;
     src = dst;
     dst = t;
   }
-  free(count); /* 4 passes: result is back in a */
+  /* four passes: the result is back in a */
 }
 
-/* csr_graph.cpp:11-55 */
+/* csr_graph.cpp:11-55: the reference sorts all (src, dst) pairs and drops
+ * duplicates; the same set, per source row: count arcs per row, place each
+ * arc's dst in its row, then sort + unique every row. */
 uint64_t orc_build_csr(const uint32_t* pairs, uint64_t npairs, uint64_t n,
                        int symmetrize, int drop_self_loops, uint64_t* offsets,
                        uint32_t* col) {
   for (uint64_t i = 0; i < 2 * npairs; ++i) {
     if (pairs[i] >= n) return UINT64_MAX;
   }
-  uint64_t cap = symmetrize ? 2 * npairs : npairs;
-  uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (cap ? cap : 1));
-  uint64_t* tmp = (uint64_t*)malloc(sizeof(uint64_t) * (cap ? cap : 1));
-  uint64_t k = 0;
-  for (uint64_t i = 0; i < npairs; ++i) {
-    const uint64_t a = pairs[2 * i], b = pairs[2 * i + 1];
-    if (a == b && drop_self_loops) continue;
-    keys[k++] = (a << 32) | b;
-    if (symmetrize && a != b) keys[k++] = (b << 32) | a;
-  }
-  radix_sort_u64(keys, tmp, k);
-  uint64_t m = 0;
-  for (uint64_t i = 0; i < k; ++i) {
-    if (i == 0 || keys[i] != keys[i - 1]) keys[m++] = keys[i];
-  }
   memset(offsets, 0, sizeof(uint64_t) * (n + 1));
-  for (uint64_t i = 0; i < m; ++i) {
-    offsets[(keys[i] >> 32) + 1]++;
-    col[i] = (uint32_t)(keys[i] & 0xFFFFFFFFULL);
+  for (uint64_t i = 0; i < npairs; ++i) {
+    const uint32_t a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a == b && drop_self_loops) continue;
+    offsets[a + 1]++;
+    if (symmetrize && a != b) offsets[b + 1]++;
   }
   for (uint64_t v = 0; v < n; ++v) offsets[v + 1] += offsets[v];
-  free(keys);
+  uint64_t* pos = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+  memcpy(pos, offsets, sizeof(uint64_t) * n);
+  for (uint64_t i = 0; i < npairs; ++i) {
+    const uint32_t a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a == b && drop_self_loops) continue;
+    col[pos[a]++] = b;
+    if (symmetrize && a != b) col[pos[b]++] = a;
+  }
+  free(pos);
+  /* Rows are compacted forward in place: row v's unique run is written at
+   * m <= offsets[v], its own start. */
+  uint64_t maxdeg = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    if (offsets[v + 1] - offsets[v] > maxdeg) maxdeg = offsets[v + 1] - offsets[v];
+  }
+  uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * (maxdeg ? maxdeg : 1));
+  uint64_t m = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint64_t b = offsets[v], e = offsets[v + 1];
+    sort_u32(col + b, e - b, tmp);
+    offsets[v] = m;
+    for (uint64_t k = b; k < e; ++k) {
+      if (k == b || col[k] != col[k - 1]) col[m++] = col[k];
+    }
+  }
+  offsets[n] = m;
   free(tmp);
   return m;
 }
@@ -194,7 +232,7 @@ int orc_pick_sources(uint64_t n, const uint64_t* offsets, uint32_t count,
   orc_mt64_seed(&s, seed);
   uint32_t got = 0;
   while (got < count) {
-    const uint32_t v = (uint32_t)(orc_mt64_next(&s) % n);
+    const uint32_t v = (uint32_t)(mt64_next(&s) % n);
     if (offsets[v + 1] > offsets[v]) out[got++] = v;
   }
   return 0;

@@ -3,10 +3,12 @@
 // the reference's proj/core graph layer (generator.cpp, csr_graph.cpp,
 // graph_stats.cpp, graph_io.cpp, tools/bfsbench.cpp:pick_sources), rebuilt for
 // multi-GB graphs: no O(m log m) global sort, no value-initialised buffers,
-// the mt19937_64 stream generated in twist-sized blocks on one thread while
-// other threads turn draws into edge pairs.
+// the mt19937_64 stream cut into chunks by jump-ahead (pbfs_mt64.h) and
+// generated on every host thread.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +19,7 @@
 #include <vector>
 
 #include "pbfs_internal.h"
+#include "pbfs_mt64.h"
 
 namespace pbfs {
 
@@ -40,45 +43,18 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 
 namespace {
 
-// ---------------------------------------------------------------------------
-// mt19937_64 ([rand.predef]) producing whole 312-word twists at a time. The
-// twist is split into its two dependency-free halves so the compiler
-// vectorises it; outputs are bit-identical to std::mt19937_64.
-class Mt64 {
- public:
-  static constexpr int N = 312, M = 156;
-  explicit Mt64(uint64_t seed) {
-    s_[0] = seed;
-    for (int i = 1; i < N; ++i) s_[i] = 6364136223846793005ULL * (s_[i - 1] ^ (s_[i - 1] >> 62)) + i;
+// PBFS_GEN_TIMING=1: phase times of the generator / builder on stderr.
+struct PhaseClock {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  PhaseClock() : on(std::getenv("PBFS_GEN_TIMING") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pbfs gen] %-18s %8.3f s\n", what,
+                 std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
   }
-  // Writes the next N outputs.
-  void block(uint64_t* out) {
-    constexpr uint64_t U = 0xFFFFFFFF80000000ULL, L = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
-    uint64_t* mt = s_;
-    for (int i = 0; i < N - M; ++i) {
-      const uint64_t y = (mt[i] & U) | (mt[i + 1] & L);
-      mt[i] = mt[i + M] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
-    }
-    for (int i = N - M; i < N - 1; ++i) {
-      const uint64_t y = (mt[i] & U) | (mt[i + 1] & L);
-      mt[i] = mt[i + M - N] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
-    }
-    {
-      const uint64_t y = (mt[N - 1] & U) | (mt[0] & L);
-      mt[N - 1] = mt[M - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & A);
-    }
-    for (int i = 0; i < N; ++i) {
-      uint64_t y = mt[i];
-      y ^= (y >> 29) & 0x5555555555555555ULL;
-      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-      y ^= y >> 43;
-      out[i] = y;
-    }
-  }
-
- private:
-  uint64_t s_[N];
 };
 
 // Sequential draw stream with block refills (for the small generators).
@@ -143,63 +119,87 @@ void uniform_convert(const uint64_t* draws, uint64_t samples, uint64_t n, uint32
   }
 }
 
-// generator.cpp:51-89 — the sample loop, pipelined: the calling thread fills
-// draw buffer k while `threads-1` workers convert buffer k-1 into pairs.
+// generator.cpp:51-89 — the sample loop. Sample s consumes draws
+// [s * per, (s + 1) * per) of ONE mt19937_64 stream, so the stream is cut
+// into chunks of whole samples whose start states are reached by jump-ahead
+// (pbfs_mt64.h): every host thread generates and converts its own chunks,
+// and the pairs are bit-identical to the sequential stream for any thread
+// count.
 void sample_pairs(uint32_t kind, uint32_t scale, uint32_t edge_factor, uint64_t seed,
                   unsigned threads, uint32_t* pairs) {
   const uint64_t n = uint64_t{1} << scale;
   const uint64_t samples = n * edge_factor;
   const uint32_t per = kind == PBFS_GEN_KRONECKER ? scale : 2;
-  // Batch = a whole number of samples and of twists (lcm via 312 * per).
-  const uint64_t batch_samples =
-      std::max<uint64_t>(Mt64::N, (uint64_t{1} << 20) / per / Mt64::N * Mt64::N);
-  const uint64_t batch_draws = batch_samples * per;  // multiple of 312
-  std::vector<uint64_t> buf[2] = {std::vector<uint64_t>(batch_draws),
-                                  std::vector<uint64_t>(batch_draws)};
-  Mt64 mt(seed);
   KronThresholds thr;
-  const unsigned workers = threads > 1 ? threads - 1 : 1;
-  auto convert = [&](const uint64_t* draws, uint64_t first, uint64_t count) {
-    // The workers outlive this call: capture the batch by value.
-    auto work = [=, &thr](unsigned t) {
-      const uint64_t b = first + count * t / workers;
-      const uint64_t e = first + count * (t + 1) / workers;
-      const uint64_t* d = draws + (b - first) * per;
-      if (kind == PBFS_GEN_KRONECKER) {
-        kron_convert(d, e - b, scale, thr, pairs + 2 * b);
-      } else {
-        uniform_convert(d, e - b, n, pairs + 2 * b);
-      }
-    };
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < workers; ++t) pool.emplace_back(work, t);
-    return pool;
-  };
-  std::vector<std::thread> pending;
-  uint64_t done = 0;
-  int cur = 0;
-  while (done < samples) {
-    const uint64_t count = std::min(batch_samples, samples - done);
-    const uint64_t draws = count * per;
-    uint64_t* out = buf[cur].data();
-    // Whole twists; the stream is consumed exactly `draws` deep because the
-    // last batch is the only partial one and nothing is drawn after it.
-    uint64_t produced = 0;
-    uint64_t tmp[Mt64::N];
-    while (produced + Mt64::N <= draws) {
-      mt.block(out + produced);
-      produced += Mt64::N;
-    }
-    if (produced < draws) {
+  PhaseClock jclk;
+  // Chunks: a multiple of 312 samples (so of 312 draws too), about four per
+  // thread for balance; tiny streams stay one chunk.
+  const uint64_t want = (samples + 4ull * threads - 1) / (4ull * threads);
+  uint64_t chunk = std::max<uint64_t>(Mt64::N * 16, (want + Mt64::N - 1) / Mt64::N * Mt64::N);
+  uint64_t nchunks = threads > 1 ? (samples + chunk - 1) / chunk : 1;
+  if (nchunks <= 1) chunk = samples;
+  std::vector<std::vector<uint64_t>> start(std::max<uint64_t>(nchunks, 1));
+  {
+    Mt64 mt(seed);
+    start[0].assign(mt.state(), mt.state() + Mt64::N);
+    if (nchunks > 1) {
+      // W_312 (after one twist) is on the reachable subspace; chunk k starts
+      // at draw k * chunk * per.
+      uint64_t tmp[Mt64::N];
       mt.block(tmp);
-      std::memcpy(out + produced, tmp, (draws - produced) * sizeof(uint64_t));
+      std::vector<uint64_t> cur(mt.state(), mt.state() + Mt64::N);
+      const uint64_t stride = chunk * per;
+      const std::vector<uint64_t> first = mt64_jump_poly(stride - Mt64::N);
+      const std::vector<uint64_t> step = nchunks > 2 ? mt64_jump_poly(stride) : first;
+      if (first.empty() || step.empty()) {
+        nchunks = 1;  // cannot jump: one chunk, front to back
+        chunk = samples;
+      }
+      for (uint64_t k = 1; k < nchunks; ++k) {
+        mt64_jump(cur.data(), k == 1 ? first : step);
+        start[k] = cur;
+      }
     }
-    for (auto& th : pending) th.join();
-    pending = convert(out, done, count);
-    done += count;
-    cur ^= 1;
   }
-  for (auto& th : pending) th.join();
+  jclk.mark("sample: jump setup");
+  auto run_chunk = [&](uint64_t k, std::vector<uint64_t>& buf) {
+    Mt64 mt(0);
+    std::memcpy(mt.state(), start[k].data(), Mt64::N * sizeof(uint64_t));
+    const uint64_t first = k * chunk;
+    const uint64_t count = std::min(chunk, samples - first);
+    // Batches of whole samples and whole twists (multiples of 312 samples).
+    const uint64_t batch = Mt64::N * 16;
+    buf.resize(batch * per);
+    uint64_t tmp[Mt64::N];
+    for (uint64_t done = 0; done < count;) {
+      const uint64_t cnt = std::min(batch, count - done);
+      const uint64_t draws = cnt * per;
+      uint64_t produced = 0;
+      while (produced + Mt64::N <= draws) {
+        mt.block(buf.data() + produced);
+        produced += Mt64::N;
+      }
+      if (produced < draws) {
+        mt.block(tmp);
+        std::memcpy(buf.data() + produced, tmp, (draws - produced) * sizeof(uint64_t));
+      }
+      if (kind == PBFS_GEN_KRONECKER) {
+        kron_convert(buf.data(), cnt, scale, thr, pairs + 2 * (first + done));
+      } else {
+        uniform_convert(buf.data(), cnt, n, pairs + 2 * (first + done));
+      }
+      done += cnt;
+    }
+  };
+  std::atomic<uint64_t> next{0};
+  parallel_for_threads(nchunks > 1 ? threads : 1, [&](unsigned) {
+    std::vector<uint64_t> buf;
+    for (;;) {
+      const uint64_t k = next.fetch_add(1);
+      if (k >= nchunks) break;
+      run_chunk(k, buf);
+    }
+  });
 }
 
 // Config-3 mesh (restated in oracle/pbfs_oracle.c
@@ -266,9 +266,11 @@ bool is_symmetric(const HostCsr& g, unsigned threads) {
 }  // namespace
 
 // csr_graph.cpp:11-55, restructured as a parallel bucketed counting sort:
-//   1. per-thread histograms of arcs per source bucket (2^k vertices each),
+//   1. per-thread histograms of arcs per fine source bucket (2^k vertices),
+//      grouped into coarse buckets of balanced arc counts,
 //   2. scatter (src<<32|dst) keys bucket-major,
-//   3. per bucket: sort + unique + per-row degree, dst compacted in place,
+//   3. per bucket: counting sort by row, per-row sort + unique, degrees,
+//      dst compacted in place,
 //   4. offsets by prefix sum, columns copied out bucket by bucket.
 pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, bool symmetrize,
                            bool drop_self_loops, unsigned threads, HostCsr* out,
@@ -278,6 +280,7 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
                                   " exceeds the supported maximum 2147483647");
   }
   threads = std::max(1u, std::min<unsigned>(threads, npairs / 4096 + 1));
+  PhaseClock clk;
   // Range check (csr_graph.cpp:18-24): report the first offending pair.
   std::atomic<uint64_t> bad{UINT64_MAX};
   parallel_for_threads(threads, [&](unsigned t) {
@@ -298,12 +301,16 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
                                   ") references a vertex >= " + std::to_string(n));
   }
 
+  // Fine buckets of 2^shift vertices (<= 65536 of them) for the histogram;
+  // runs of fine buckets are grouped into coarse buckets of about
+  // total / (16 threads) arcs each, so RMAT's low-id hub region (several % of
+  // all arcs in a few thousand vertices) is not one thread's straggler.
   int shift = 0;
-  while ((n >> shift) > 4096) ++shift;  // <= 4096 buckets
-  const uint64_t nbuckets = n ? ((n - 1) >> shift) + 1 : 1;
-  std::vector<uint64_t> hist(static_cast<size_t>(threads) * nbuckets, 0);
+  while ((n >> shift) > 65536) ++shift;
+  const uint64_t nfine = n ? ((n - 1) >> shift) + 1 : 1;
+  std::vector<uint64_t> fine(static_cast<size_t>(threads) * nfine, 0);
   parallel_for_threads(threads, [&](unsigned t) {
-    uint64_t* h = hist.data() + t * nbuckets;
+    uint64_t* h = fine.data() + t * nfine;
     const uint64_t b = npairs * t / threads, e = npairs * (t + 1) / threads;
     for (uint64_t i = b; i < e; ++i) {
       const uint32_t s = pairs[2 * i], d = pairs[2 * i + 1];
@@ -315,7 +322,35 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
       if (symmetrize) ++h[d >> shift];
     }
   });
+  uint64_t total = 0;
+  std::vector<uint64_t> fine_sum(nfine, 0);
+  for (unsigned t = 0; t < threads; ++t) {
+    for (uint64_t f = 0; f < nfine; ++f) fine_sum[f] += fine[t * nfine + f];
+  }
+  for (uint64_t f = 0; f < nfine; ++f) total += fine_sum[f];
+  const uint64_t target = std::max<uint64_t>(total / (16ull * threads) + 1, 1ull << 16);
+  std::vector<uint32_t> f2c(nfine);
+  std::vector<uint64_t> cv0;  // first vertex of each coarse bucket (+ n at the end)
+  {
+    uint64_t acc = 0;
+    for (uint64_t f = 0; f < nfine; ++f) {
+      if (f == 0 || acc >= target) {
+        cv0.push_back(f << shift);
+        acc = 0;
+      }
+      f2c[f] = static_cast<uint32_t>(cv0.size() - 1);
+      acc += fine_sum[f];
+    }
+    cv0.push_back(n);
+  }
+  const uint64_t nbuckets = cv0.size() - 1;
   // bucket-major, thread-minor positions
+  std::vector<uint64_t> hist(static_cast<size_t>(threads) * nbuckets, 0);
+  for (unsigned t = 0; t < threads; ++t) {
+    for (uint64_t f = 0; f < nfine; ++f) hist[t * nbuckets + f2c[f]] += fine[t * nfine + f];
+  }
+  fine.clear();
+  fine.shrink_to_fit();
   std::vector<uint64_t> bucket_start(nbuckets + 1, 0);
   {
     uint64_t run = 0;
@@ -329,7 +364,6 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
     }
     bucket_start[nbuckets] = run;
   }
-  const uint64_t total = bucket_start[nbuckets];
   std::unique_ptr<uint64_t[], FreeDeleter> keys(
       static_cast<uint64_t*>(std::malloc((total ? total : 1) * sizeof(uint64_t))));
   if (!keys) return fail(PBFS_E_CAPACITY, "host allocation failed for " + std::to_string(total) + " arcs");
@@ -339,15 +373,16 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
     for (uint64_t i = b; i < e; ++i) {
       const uint64_t s = pairs[2 * i], d = pairs[2 * i + 1];
       if (s == d) {
-        if (!drop_self_loops) keys[pos[s >> shift]++] = (s << 32) | d;
+        if (!drop_self_loops) keys[pos[f2c[s >> shift]]++] = (s << 32) | d;
         continue;
       }
-      keys[pos[s >> shift]++] = (s << 32) | d;
-      if (symmetrize) keys[pos[d >> shift]++] = (d << 32) | s;
+      keys[pos[f2c[s >> shift]]++] = (s << 32) | d;
+      if (symmetrize) keys[pos[f2c[d >> shift]]++] = (d << 32) | s;
     }
   });
   hist.clear();
   hist.shrink_to_fit();
+  clk.mark("build: scatter");
   // Peak host memory at RMAT-28 is pairs + keys; the pairs are dead from here.
   if (owned_pairs) owned_pairs->reset();
 
@@ -355,30 +390,59 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
   out->offsets.reset(new (std::nothrow) uint64_t[n + 1]);
   if (!out->offsets) return fail(PBFS_E_CAPACITY, "host allocation failed (offsets)");
   std::vector<uint64_t> bucket_unique(nbuckets, 0);
+  // Largest buckets first (dynamic assignment balances the tail).
+  std::vector<uint64_t> order(nbuckets);
+  for (uint64_t bk = 0; bk < nbuckets; ++bk) order[bk] = bk;
+  std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) {
+    return bucket_start[x + 1] - bucket_start[x] > bucket_start[y + 1] - bucket_start[y];
+  });
   std::atomic<uint64_t> next_bucket{0};
   uint32_t* colbuf = reinterpret_cast<uint32_t*>(keys.get());
+  // Per bucket: counting sort of its keys by source row (the degrees go
+  // straight into offsets[v+1]), then each row's destinations sorted and
+  // deduplicated (sort + unique per row = the reference's global pair sort
+  // + unique, csr_graph.cpp:35-36) and compacted as u32 at the start of the
+  // bucket's own key range, which has been fully read by then.
   parallel_for_threads(threads, [&](unsigned) {
+    std::vector<uint32_t> tmp;
+    std::vector<uint64_t> pos;
     for (;;) {
-      const uint64_t bk = next_bucket.fetch_add(1);
-      if (bk >= nbuckets) break;
-      uint64_t* kb = keys.get() + bucket_start[bk];
-      uint64_t* ke = keys.get() + bucket_start[bk + 1];
-      std::sort(kb, ke);
-      ke = std::unique(kb, ke);
-      const uint64_t cnt = static_cast<uint64_t>(ke - kb);
-      bucket_unique[bk] = cnt;
-      const uint64_t v0 = bk << shift, v1 = std::min<uint64_t>(n, (bk + 1) << shift);
-      for (uint64_t v = v0; v < v1; ++v) out->offsets[v + 1] = 0;
-      // Degrees into offsets[v+1]; destinations compacted in place as u32
-      // (write index 4i never passes read index 8i).
-      uint32_t* cdst = colbuf + 2 * bucket_start[bk];
-      for (uint64_t i = 0; i < cnt; ++i) {
-        const uint64_t k = kb[i];
-        ++out->offsets[(k >> 32) + 1];
-        cdst[i] = static_cast<uint32_t>(k);
+      const uint64_t oi = next_bucket.fetch_add(1);
+      if (oi >= nbuckets) break;
+      const uint64_t bk = order[oi];
+      const uint64_t* kb = keys.get() + bucket_start[bk];
+      const uint64_t K = bucket_start[bk + 1] - bucket_start[bk];
+      const uint64_t v0 = cv0[bk], v1 = cv0[bk + 1];
+      uint64_t* deg = out->offsets.get() + v0 + 1;
+      const uint64_t rows = v1 - v0;
+      std::fill(deg, deg + rows, 0);
+      for (uint64_t i = 0; i < K; ++i) ++deg[(kb[i] >> 32) - v0];
+      pos.resize(rows);
+      uint64_t run = 0;
+      for (uint64_t j = 0; j < rows; ++j) {
+        pos[j] = run;
+        run += deg[j];
       }
+      tmp.resize(K);
+      for (uint64_t i = 0; i < K; ++i) tmp[pos[(kb[i] >> 32) - v0]++] = static_cast<uint32_t>(kb[i]);
+      uint32_t* cdst = colbuf + 2 * bucket_start[bk];
+      uint64_t out_i = 0;
+      for (uint64_t j = 0; j < rows; ++j) {
+        uint32_t* rb = tmp.data() + pos[j] - deg[j];
+        uint32_t* re = tmp.data() + pos[j];
+        if (re - rb > 1) {
+          std::sort(rb, re);
+          re = std::unique(rb, re);
+        }
+        const uint64_t u = static_cast<uint64_t>(re - rb);
+        std::memcpy(cdst + out_i, rb, u * sizeof(uint32_t));
+        out_i += u;
+        deg[j] = u;
+      }
+      bucket_unique[bk] = out_i;
     }
   });
+  clk.mark("build: sort+unique");
   // Offsets: bucket bases, then rows (parallel per bucket).
   std::vector<uint64_t> bucket_base(nbuckets + 1, 0);
   for (uint64_t bk = 0; bk < nbuckets; ++bk) bucket_base[bk + 1] = bucket_base[bk] + bucket_unique[bk];
@@ -390,7 +454,7 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
     for (;;) {
       const uint64_t bk = next_bucket.fetch_add(1);
       if (bk >= nbuckets) break;
-      const uint64_t v0 = bk << shift, v1 = std::min<uint64_t>(n, (bk + 1) << shift);
+      const uint64_t v0 = cv0[bk], v1 = cv0[bk + 1];
       uint64_t run = bucket_base[bk];
       for (uint64_t v = v0; v < v1; ++v) {
         run += out->offsets[v + 1];
@@ -409,6 +473,7 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
   if (!shrunk) return fail(PBFS_E_CAPACITY, "host reallocation failed (columns)");
   keys.release();
   out->col.reset(static_cast<uint32_t*>(shrunk));
+  clk.mark("build: offsets+cols");
   out->symmetric = symmetrize ? true : is_symmetric(*out, threads);
   return PBFS_OK;
 }
@@ -545,7 +610,9 @@ pbfs_status pbfs_generate(const pbfs_gen_spec* spec, pbfs_host_csr** out) {
     if (!raw) {
       return fail(PBFS_E_CAPACITY, "host allocation failed for " + std::to_string(samples) + " samples");
     }
+    PhaseClock clk;
     sample_pairs(spec->kind, spec->scale, spec->edge_factor, spec->seed, threads, raw.get());
+    clk.mark("sample pairs");
     return build_to_handle(raw.get(), samples, n, spec->drop_self_loops, threads, out, &raw);
   } else {
     return fail(PBFS_E_CONFIG, "unknown generator kind");

@@ -1,8 +1,11 @@
-"""BASELINE.json configs on the B200: config 1 (RMAT-20, int32 offsets) for
-all 64 seeded sources against the oracle's serial BFS, configs 2-3 (ER 2^24,
-4096^2 mesh) on seeded sources, plus size-independent BFS properties
-(checked vectorised over every arc) that also cover RMAT-26 when
-PBFS_TEST_LARGE=1."""
+"""BASELINE.json configs on the B200, every one at full size in the default
+GPU run: config 1 (RMAT-20, int32 offsets) for all 64 seeded sources against
+the oracle's serial BFS; configs 2-5 (ER 2^24, 4096^2 mesh, RMAT-26,
+RMAT-28) on budgeted subsets of the bench's seeded sources against the
+reference's own parbfs::bfs_hybrid (oracle/_ref, all host threads) --
+distances, per-level phases and distinct sizes; plus size-independent BFS
+properties (checked vectorised over every arc). PBFS_TEST_LARGE=1 widens
+every config to all 64 sources."""
 import os
 
 import numpy as np
@@ -76,20 +79,73 @@ def test_config1_rmat20_all_64_sources(port):
     bfs_properties(g, got, int(s))
 
 
+def _ref_graph(g):
+    import oracle
+    assert oracle.ref_available(), "oracle/_ref (the reference library) must travel with the repo"
+    ref = oracle.ref()
+    return ref, ref.from_csr(g.row_offsets.astype(np.uint64, copy=False), g.column_indices, True)
+
+
+def _check_against_reference(g, dg, srcs, cfg, variant=3):
+    """Distances, per-level phases and distinct sizes equal the reference's
+    own parbfs::bfs_hybrid (variant 3) / bfs_hybrid_beamer (4) on all host
+    threads -- acceptance.cpp:112-147's equivalence gate at full size."""
+    ref, rg = _ref_graph(g)
+    for i, s in enumerate(srcs):
+        r = dg.bfs(s, cfg)
+        want, recs, _ = ref.run(rg, s, variant, workers=os.cpu_count() or 1,
+                                force_td=cfg.force_top_down_only)
+        assert np.array_equal(r.distances, want), (i, s)
+        assert [(x.depth, int(x.phase), x.distinct_size) for x in r.trace.records] == \
+            [(x["depth"], x["phase"], x["distinct_size"]) for x in recs], (i, s)
+    del rg
+
+
+@pytest.fixture(scope="module")
+def rmat26():
+    g, offb = config_graph("rmat26")
+    dg = g.device(0, offb)
+    yield g, dg
+    g.release_device()
+
+
+def test_config4_rmat26_16_sources_vs_reference_hybrid(rmat26):
+    # The first 16 of the bench's 64 seeded sources (pick_sources, seed 1).
+    g, dg = rmat26
+    cfg = dispatch_config(g)
+    assert not cfg.force_top_down_only
+    srcs = [int(s) for s in pb.pick_sources(g, 64, 1)][:16]
+    _check_against_reference(g, dg, srcs, cfg)
+
+
+def test_config4_rmat26_beamer_vs_reference_beamer(rmat26):
+    g, dg = rmat26
+    srcs = [int(s) for s in pb.pick_sources(g, 64, 1)][16:20]
+    _check_against_reference(g, dg, srcs, pb.KernelConfig(variant=pb.KernelVariant.HybridBeamer),
+                             variant=4)
+
+
 @pytest.mark.parametrize("name", ["er24", "mesh4096"])
-def test_config2_config3_seeded_sources(name, port):
+def test_config2_config3_16_sources_vs_reference_hybrid(name):
     g, offb = config_graph(name)
     dg = g.device(0, offb)
     cfg = dispatch_config(g)
     if name == "mesh4096":
         assert cfg.force_top_down_only  # avg degree ~3.6 -> the dispatcher's TD-only path
-    for s in pb.pick_sources(g, 3, 1):
-        want = port.bfs_serial(g.row_offsets, g.column_indices, int(s))
-        r = dg.bfs(int(s), cfg)
-        assert np.array_equal(r.distances, want), (name, int(s))
-        assert sum(rec.distinct_size for rec in r.trace.records) == \
-            int((want != UNREACHED).sum())
-    bfs_properties(g, r.distances, int(s))
+    srcs = [int(s) for s in pb.pick_sources(g, 64, 1)][:16]
+    _check_against_reference(g, dg, srcs, cfg)
+    bfs_properties(g, dg.bfs(srcs[-1], cfg).distances, srcs[-1])
+    g.release_device()
+
+
+def test_config5_rmat28_4_sources_vs_reference_hybrid():
+    # 8.6 G arcs: generation (jump-ahead parallel), 38 GB resident on one
+    # B200, four bench sources against the reference's bfs_hybrid.
+    g, offb = config_graph("rmat28")
+    dg = g.device(0, offb)
+    cfg = dispatch_config(g)
+    srcs = [int(s) for s in pb.pick_sources(g, 64, 1)][:4]
+    _check_against_reference(g, dg, srcs, cfg)
     g.release_device()
 
 

@@ -220,3 +220,18 @@ def test_trace_helpers():
     assert lines[0] == ("run_id,variant,source,depth,phase,frontier_size,distinct_size,"
                         "duplicate_count,edges_examined,flush_events,elapsed_ns")
     assert lines[2] == "r1,hybrid,3,1,bottom-up,4,2,2,7,0,20"
+
+
+@pytest.mark.parametrize("kind,scale,ef", [(pb.GeneratorKind.Kronecker, 17, 8),
+                                           (pb.GeneratorKind.UniformRandom, 16, 16)])
+def test_parallel_generation_equals_one_stream(kind, scale, ef):
+    # The stream is cut into chunks whose start states come from mt19937_64
+    # jump-ahead (pbfs_mt64.cpp); any thread count must give the graph the
+    # single sequential stream gives (threads=1 never jumps), and the
+    # reference's own generate() (pinned by the digests above).
+    spec = pb.GeneratorSpec(kind, scale, ef, 77, drop_self_loops=True)
+    one = pb.generate(spec, threads=1)
+    for t in (2, 3, 8):
+        g = pb.generate(spec, threads=t)
+        assert np.array_equal(g.row_offsets, one.row_offsets), t
+        assert np.array_equal(g.column_indices, one.column_indices), t
