@@ -224,6 +224,16 @@ struct Params {
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// The CTAs one traversal runs on: the whole launch (single-GPU engine), or
+// one partition's share of a launch that carries several partitions of the
+// multi-partition engine (pbfs_multi.cu). Every work-distribution loop and
+// the grid barrier take it instead of reading blockIdx / gridDim.
+struct VGrid {
+  unsigned cta;   // this CTA's index among the traversal's CTAs
+  unsigned ctas;  // CTAs of the traversal
+};
+__device__ __forceinline__ VGrid hw_grid() { return VGrid{blockIdx.x, gridDim.x}; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -318,13 +328,14 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 struct GridBarrier {
   Ctl* ctl;
   unsigned long long* snap;  // shared memory, 8 x u64
+  VGrid vg = hw_grid();
   // `src` (optional, 64 B, 16 B aligned): thread 0 copies it into `snap`
   // after the barrier, so a CTA reads the level counters with one request
   // instead of every thread polling the same L2 line.
   __device__ __forceinline__ void sync(const void* src = nullptr) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      const unsigned nb = vg.cta == 0 ? 0x80000000u - (vg.ctas - 1) : 1u;
       unsigned old;
       asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;"
                    : "=r"(old) : "l"(&ctl->bar_word), "r"(nb) : "memory");
@@ -568,17 +579,18 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
 template <int C, typename OffT>
 __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint32_t* qin,
                                unsigned long long qlen, uint32_t* qout, WarpPush& wp,
-                               LevelCnt* cnt, WarpTally& t, uint32_t* obm, uint32_t* stale) {
+                               LevelCnt* cnt, WarpTally& t, uint32_t* obm, uint32_t* stale,
+                               VGrid vg = hw_grid()) {
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
-  const unsigned warps_total = gridDim.x * kWarps;
+  const unsigned warps_total = vg.ctas * kWarps;
   // Slice width: 32 frontier vertices per warp, fewer on a frontier smaller
   // than one full slice per warp, so its edges spread over more warps instead
   // of queueing up as batches (each a dependent round-trip chain) in a few.
   uint32_t W = 32;
   while (W > 1 && (unsigned long long)warps_total * (W / 2) >= qlen) W /= 2;
-  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * W;
+  unsigned long long base = (unsigned long long)(vg.cta * kWarps + (threadIdx.x >> 5)) * W;
   while (base < qlen) {
     const unsigned long long i = base + lane;
     OffT beg = 0, end = 0;
@@ -642,13 +654,13 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
 template <int C, typename OffT>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
                                uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t,
-                               uint32_t* obm) {
+                               uint32_t* obm, VGrid vg = hw_grid()) {
   constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
-  const unsigned warps_total = gridDim.x * kWarps;
-  unsigned int it = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const unsigned warps_total = vg.ctas * kWarps;
+  unsigned int it = vg.cta * kWarps + (threadIdx.x >> 5);
   while (it < items) {
     const HeavyItem h = p.heavy[it];
     const uint32_t* base = p.col + h.beg;
@@ -838,14 +850,14 @@ __device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const ui
 template <int GPT, typename OffT>
 __device__ void bu_phase_t(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
                            uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
-                           unsigned int* cursor) {
+                           unsigned int* cursor, VGrid vg) {
   constexpr bool sparse = GPT > 1;
   constexpr int KB = kBuSlots;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
-  const unsigned warps_total = gridDim.x * kWarps;
-  const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const unsigned warps_total = vg.ctas * kWarps;
+  const unsigned gw = vg.cta * kWarps + (threadIdx.x >> 5);
   const uint32_t groups = (p.words + 31) / 32;
   constexpr uint32_t gpt = GPT;
   const uint32_t tasks = (groups + gpt - 1) / gpt;
@@ -1050,11 +1062,11 @@ template <typename OffT>
 __device__ __forceinline__ void bu_phase(const Params<OffT>& p, uint32_t depth,
                                          const uint32_t* front, uint32_t* next, uint32_t* list,
                                          uint32_t* found, WarpTally& t, unsigned int* cursor,
-                                         bool sparse) {
+                                         bool sparse, VGrid vg = hw_grid()) {
   if (sparse) {
-    bu_phase_t<kBuSparseGroups>(p, depth, front, next, list, found, t, cursor);
+    bu_phase_t<kBuSparseGroups>(p, depth, front, next, list, found, t, cursor, vg);
   } else {
-    bu_phase_t<1>(p, depth, front, next, list, found, t, cursor);
+    bu_phase_t<1>(p, depth, front, next, list, found, t, cursor, vg);
   }
 }
 
@@ -1088,10 +1100,10 @@ __device__ __forceinline__ void warp_flush_tally(LevelCnt* cnt, WarpTally& t, bo
 template <int CW>
 __device__ __forceinline__ void compact_bitmap_cw(uint32_t* nb, uint32_t* q, uint32_t words,
                                                   unsigned int* counter, bool clear,
-                                                  uint32_t* zero_other) {
+                                                  uint32_t* zero_other, VGrid vg) {
   const unsigned lane = lane_id();
-  const unsigned warps_total = gridDim.x * kWarps;
-  const unsigned gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const unsigned warps_total = vg.ctas * kWarps;
+  const unsigned gw = vg.cta * kWarps + (threadIdx.x >> 5);
   for (uint32_t base = gw * 32 * CW; base < words; base += warps_total * 32 * CW) {
     uint32_t wd[CW];
     uint32_t c = 0;
@@ -1135,11 +1147,12 @@ __device__ __forceinline__ void compact_bitmap_cw(uint32_t* nb, uint32_t* q, uin
 // bitmaps one word per lane keeps the bit extraction spread over the grid.
 __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32_t words,
                                                unsigned int* counter, bool clear,
-                                               uint32_t* zero_other = nullptr, bool wide = false) {
-  if (wide || words >= gridDim.x * kWarps * 32u * 8u) {
-    compact_bitmap_cw<8>(nb, q, words, counter, clear, zero_other);
+                                               uint32_t* zero_other = nullptr, bool wide = false,
+                                               VGrid vg = hw_grid()) {
+  if (wide || words >= vg.ctas * kWarps * 32u * 8u) {
+    compact_bitmap_cw<8>(nb, q, words, counter, clear, zero_other, vg);
   } else {
-    compact_bitmap_cw<1>(nb, q, words, counter, clear, zero_other);
+    compact_bitmap_cw<1>(nb, q, words, counter, clear, zero_other, vg);
   }
 }
 
@@ -1152,9 +1165,9 @@ __device__ __forceinline__ void compact_bitmap(uint32_t* nb, uint32_t* q, uint32
 __device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dist, uint32_t nd,
                                                 uint32_t* out, uint32_t words,
                                                 unsigned long long n, const uint32_t* visited,
-                                                const uint32_t* init_mask) {
-  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+                                                const uint32_t* init_mask, VGrid vg = hw_grid()) {
+  const unsigned long long nthreads = (unsigned long long)vg.ctas * blockDim.x;
+  for (unsigned long long w = (unsigned long long)vg.cta * blockDim.x + threadIdx.x;
        w < words; w += nthreads) {
     const unsigned long long base = w * 32;
     uint32_t bits = 0;

@@ -43,42 +43,14 @@
 
 #include "pbfs_internal.h"
 #include "pbfs_kernels.cuh"
+#include "pbfs_part_impl.h"
 
 using namespace pbfs;
 using namespace pbfs::dev;
+using namespace pbfs::part;
 
 
 namespace {
-
-// ---- relabel pi on [0, 2^k) ---------------------------------------------------
-struct Relabel {
-  uint32_t k = 0;       // n_pad = 2^k when hashed
-  uint32_t hashed = 0;  // 0: identity
-  uint64_t mask = 0;
-  uint64_t a = 0, b = 0;
-  uint32_t h = 0;
-};
-
-
-Relabel make_relabel(uint32_t k, bool hashed) {
-  Relabel r;
-  r.k = k;
-  r.hashed = hashed && k >= 2;
-  r.mask = k >= 64 ? ~0ull : ((1ull << k) - 1);
-  r.a = 0x9E3779B97F4A7C15ull & r.mask;
-  r.b = 0xC2B2AE3D27D4EB4Full & r.mask;
-  r.a |= 1;
-  r.b |= 1;
-  r.h = (k + 1) / 2;  // 2h >= k: x ^= x >> h is its own inverse
-  return r;
-}
-
-__host__ __device__ __forceinline__ uint64_t pi_fwd(const Relabel& r, uint64_t v) {
-  if (!r.hashed) return v;
-  uint64_t x = (v * r.a) & r.mask;
-  x ^= x >> r.h;
-  return (x * r.b) & r.mask;
-}
 
 // ---- partition-build kernels ---------------------------------------------------
 // Ownership: rank of v = pi(v) / nloc (the hash balances RMAT's arcs).
@@ -226,16 +198,6 @@ __global__ void k_local_mask(const unsigned long long* __restrict__ rowloc, uint
 // k_decide (one thread) applies the 5 % rule. The host's only per-level
 // knowledge is the bitmap parity (fcur flips every level), which names the
 // `next` buffer it allgathers.
-constexpr uint32_t kPartRecCap = 1u << 16;  // device level records kept per traversal
-
-struct PartState {
-  unsigned long long qlen;          // current top-down queue length
-  unsigned long long distinct;      // popcount of the gathered next bitmap
-  unsigned long long cur_distinct;  // current frontier size
-  unsigned int td, fcur, depth, done, compact;
-  unsigned int pad[3];
-};
-
 __global__ void k_begin(uint32_t* dist, uint32_t* visited, const uint32_t* mask, uint64_t nloc,
                         uint64_t lwords, uint32_t* front, uint32_t* next, uint64_t clear_lo,
                         uint64_t clear_words, const uint32_t* __restrict__ gid, uint32_t source,
@@ -397,51 +359,6 @@ __global__ void k_unrelabel(const uint32_t* __restrict__ dist_pi, uint64_t n,
 
 }  // namespace
 
-struct pbfs_part {
-  int device = 0;
-  uint32_t rank = 0, world = 1;
-  cudaStream_t stream = nullptr;
-  Relabel rl;
-  uint64_t n = 0, npad = 0, nloc = 0, lo = 0;
-  uint64_t words_total = 0, lwords = 0;
-  uint64_t m_loc = 0;
-  uint32_t offb = 8;
-  bool shared = false;
-  int grid = 0;
-  // row slice (bottom-up)
-  unsigned long long* rowloc = nullptr;  // nloc + 1
-  uint32_t* colrow = nullptr;            // m_loc, global pi-ids
-  uint32_t* first = nullptr;             // nloc + 1: first row-slice neighbour
-  // order-preserving numbering (k_owner_gid): vertex -> gid, gid -> vertex
-  uint32_t* gid = nullptr;               // n
-  uint32_t* inv = nullptr;               // npad (0xFFFFFFFF = padding)
-  std::vector<uint32_t> gid_host;        // lazily copied for pbfs_part_unrelabel_host
-  // column slice (top-down)
-  unsigned long long* colptr = nullptr;  // npad + 1
-  uint32_t* colcol = nullptr;            // m_loc, local ids
-  uint64_t col_maxdeg = 0, heavy_cap = 0;
-  size_t persist = 0;  // persisting-L2 set-aside available to the level kernels
-  // traversal state
-  uint32_t* dist = nullptr;      // nloc
-  uint32_t* visited = nullptr;   // lwords
-  uint32_t* mask = nullptr;      // lwords
-  uint32_t* bm[2] = {nullptr, nullptr};  // full bitmaps (own or shared)
-  int fcur = 0;                  // bm[fcur] = current frontier, bm[fcur^1] = next
-  uint32_t* queue[2] = {nullptr, nullptr};
-  HeavyItem* heavy = nullptr;
-  Ctl* ctl = nullptr;
-  PartState* st = nullptr;
-  PartState* st_host = nullptr;  // pinned mirror
-  std::vector<void*> allocs;
-  pbfs_level* recs = nullptr;    // device, kPartRecCap level records
-  // host mirror of the level state (identical on every rank)
-  uint32_t issued = 0;           // levels enqueued since begin
-  uint32_t depth = 0;
-  bool td = true;
-  int policy = kPolicyFraction;
-  double threshold = 0.05;
-};
-
 namespace {
 
 pbfs_status cuda_fail_p(cudaError_t e, const char* what) {
@@ -467,14 +384,7 @@ pbfs_status palloc(pbfs_part* g, T** p, size_t bytes) {
   return PBFS_OK;
 }
 
-void part_release(pbfs_part* g) {
-  if (!g) return;
-  cudaSetDevice(g->device);
-  for (void* p : g->allocs) cudaFree(p);
-  if (g->st_host) cudaFreeHost(g->st_host);
-  if (g->stream) cudaStreamDestroy(g->stream);
-  delete g;
-}
+void part_release(pbfs_part* g) { pbfs::part::release(g); }
 
 // Launch on `s` with a persisting-L2 window over [base, base + bytes): the
 // top-down kernels keep the local visited slice resident against the col
@@ -501,6 +411,20 @@ cudaError_t launch_window(void (*kern)(KArgs...), int grid, cudaStream_t s, cons
   lc.attrs = attr;
   lc.numAttrs = nattr;
   return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace
+
+namespace pbfs {
+namespace part {
+
+void release(pbfs_part* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  for (void* p : g->allocs) cudaFree(p);
+  if (g->st_host) cudaFreeHost(g->st_host);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
 }
 
 Params<unsigned long long> td_params(const pbfs_part* g) {
@@ -536,6 +460,11 @@ Params<unsigned long long> bu_params(const pbfs_part* g) {
   p.threshold = g->threshold;
   return p;
 }
+
+}  // namespace part
+}  // namespace pbfs
+
+namespace {
 
 template <typename OffT>
 pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* col) {
@@ -631,6 +560,15 @@ pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void*
                              const uint32_t* col, uint32_t offb, const pbfs_part_options* opt,
                              pbfs_part** out);
 }  // namespace
+
+namespace pbfs {
+namespace part {
+pbfs_status create(uint64_t n, bool symmetric, int device, const void* rowptr, const uint32_t* col,
+                   uint32_t offb, const pbfs_part_options* opt, pbfs_part** out) {
+  return part_create_impl(n, symmetric, device, rowptr, col, offb, opt, out);
+}
+}  // namespace part
+}  // namespace pbfs
 
 extern "C" {
 
