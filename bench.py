@@ -380,8 +380,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--partitions", type=int, default=0,
                     help="on one GPU: run the partitioned engine with this many loopback "
-                         "partitions (tests the multi-GPU path; N>1 under torchrun always "
-                         "partitions)")
+                         "partitions (tests the multi-GPU path)")
+    ap.add_argument("--engine", default="fused", choices=["fused", "levels"],
+                    help="multi-GPU engine: fused (pbfs_multi: one persistent launch per "
+                         "device, exchange over peer memory inside the level kernels; one "
+                         "process drives every GPU) or levels (pbfs_part: one process per "
+                         "GPU, per-level launches + NCCL allgather)")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -396,10 +400,159 @@ def main():
         run_reference_arm(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.partitions > 1:
+    if args.engine == "fused" and (args.gpus > 1 or args.partitions > 1):
+        # One process drives every GPU (peer access over NVLink); under
+        # torchrun the other ranks only join the barrier.
+        run_multi(args, world)
+    elif world > 1 or args.partitions > 1:
         run_partitioned(args)
+    elif args.gpus > 1:
+        # --engine levels without torchrun: spawn one rank per GPU.
+        spawn_ranks(args)
     else:
         run_single(args)
+
+
+def spawn_ranks(args):
+    """bench.py --gpus N --engine levels started without torchrun: launch the
+    N ranks ourselves (torch.distributed.run, 127.0.0.1) and relay rank 0's
+    line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", "--master-port=29533",
+           os.path.abspath(__file__)] + [a for a in sys.argv[1:]]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+def run_multi(args, world):
+    """pbfs_multi over N GPUs (or G loopback partitions on one GPU): one
+    persistent launch per device per traversal, frontier exchange fused into
+    the level kernels. value = harmonic mean of E_r / t with t the device
+    span (first device's start to the last device's end) per traversal."""
+    import torch
+    import paper_2503_00430_b200 as pb
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo")
+        if rank != 0:
+            tdist.barrier()
+            tdist.destroy_process_group()
+            return
+    if args.partitions > 1:
+        devices = [0] * args.partitions
+        n_gpus = 1
+    else:
+        ndev = torch.cuda.device_count()
+        if ndev < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but only {ndev} CUDA devices are visible")
+        devices = list(range(args.gpus))
+        n_gpus = args.gpus
+    torch.cuda.set_device(0)
+    graph = build_graph(args.workload)
+    cfg, _ = kernel_config(graph)
+    cfg.variant = pb.KernelVariant.Hybrid
+    t0 = time.time()
+    mg = graph.multi_device(devices)
+    build_s = time.time() - t0
+    log(f"[bench] {len(devices)} partitions on devices {devices} built in {build_s:.1f}s, "
+        f"{mg.info['ctas_per_partition']} CTAs each, local arcs {mg.info['local_arcs']}")
+    dg0 = None
+    if args.workload == "mesh4096":
+        dg0 = graph.device(0, 8)
+    sources = [int(s) for s in choose_sources(graph, dg0, cfg, args.workload)] \
+        if dg0 is not None else [int(s) for s in pb.pick_sources(graph, NUM_SOURCES, SOURCE_SEED)]
+    if dg0 is not None:
+        graph.release_device()
+    n = graph.vertex_count
+    e_r, b_alg = {}, {}
+    for s in sources:
+        mg.bfs_async(s, cfg)
+        mg.sync()
+        nr, ar = mg.component()
+        e_r[s] = ar / 2.0
+        b_alg[s] = 4.0 * ar + 2.0 * 8 * nr + 4.0 * n
+    flushes = [torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{d}")
+               for d in sorted(set(devices))]
+
+    def flush_all():
+        for f in flushes:
+            f.zero_()
+        for d in sorted(set(devices)):
+            torch.cuda.synchronize(d)
+
+    for _ in range(args.warmup):
+        for s in sources:
+            mg.bfs_async(s, cfg)
+    mg.sync()
+    times = {s: [] for s in sources}
+    launches = 0
+    with ClockSampler(0) as clocks:
+        time.sleep(1.0)
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            for s in sources:
+                flush_all()
+                mg.bfs_async(s, cfg)
+                times[s].append(mg.sync())
+                launches += len(set(devices))
+        wall_ms = (time.perf_counter() - t_all) * 1e3
+    clk = clocks.summary()
+    t_src = {s: statistics.mean(v) for s, v in times.items()}
+    gteps = [e_r[s] / (t_src[s] * 1e-3) / 1e9 for s in sources]
+    value = harmonic(gteps)
+    achieved = sum(b_alg.values()) / sum(t * 1e-3 for t in t_src.values()) / 1e9
+    peak, _ = _peak_and_traffic(args.workload)
+    # e2e: the public call with host buffers -- pbfs_multi_bfs gathers the
+    # partitions' distances on device 0 (peer copies), maps them back to
+    # vertex ids there and copies them to pinned host memory.
+    host = pb.parbfs.pinned_empty(n, np.uint32)
+    e2e_rows = []
+    for s in sources:
+        flush_all()
+        t0 = time.perf_counter()
+        mg.bfs(s, cfg, want_trace=False, out=host)
+        e2e_rows.append(e_r[s] / (time.perf_counter() - t0) / 1e9)
+    e2e_value = harmonic(e2e_rows)
+    import oracle
+    want = oracle.port().bfs_serial(graph.row_offsets.astype(np.uint64, copy=False),
+                                    graph.column_indices, sources[-1])
+    e2e_parity = bool(np.array_equal(host, want))
+    peak_all = peak * n_gpus
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall_ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {**workload_config_raw(args, n, graph.edge_count),
+                   "parallelism": (f"{len(devices)} loopback partitions on one GPU in one launch "
+                                   "(fused exchange path test)" if n_gpus == 1 else
+                                   f"1D vertex partition over {n_gpus} GPUs, one process, one "
+                                   "persistent launch per GPU, frontier exchange over NVLink peer "
+                                   "stores + flag round per level"),
+                   "engine": "pbfs_multi (fused)", "partitions": len(devices),
+                   "partition_build_s": round(build_s, 2),
+                   "l2": "flushed (512 MiB memset per device) between traversals",
+                   "mean_bfs_ms": round(statistics.mean(t_src.values()), 4)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_all,
+                     "unit": "GB/s", "frac": round(achieved / peak_all, 4), "traffic": None,
+                     "kernel": "bfs_multi (one cooperative launch per device per BFS)",
+                     "bytes_model": "B_alg = 4*A_r + 2*8*N_r + 4*N per source"},
+        "cpu_baseline": None,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4 * len(sources),
+                "d2h_bytes_per_step": 4 * n * len(sources),
+                "note": "pbfs_multi_bfs per source: traversal + peer gather of the distance "
+                        "slices + device un-relabel + pinned D2H",
+                "parity_vs_oracle_last_source": e2e_parity},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+        tdist.destroy_process_group()
 
 
 def run_single(args):

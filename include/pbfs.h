@@ -349,6 +349,56 @@ pbfs_status pbfs_part_unrelabel(pbfs_part* p, const uint32_t* dist_pi, uint32_t*
 pbfs_status pbfs_part_copy_dist(pbfs_part* p, uint32_t* host_out);
 pbfs_status pbfs_part_unrelabel_host(const pbfs_part* p, const uint32_t* dist_pi, uint32_t* dist);
 
+/* ---- multi-partition engine: the exchange fused into the level kernels ----
+ * The same 1D vertex partition, run as ONE persistent cooperative launch per
+ * device for a whole traversal (pbfs_multi.cu). Partition i lives on
+ * devices[i]; partitions on one device (listed contiguously) share that
+ * device's launch, so devices = {0, 0, 0, 0} runs four partitions on one
+ * GPU through exactly the exchange code that devices = {0, 1, 2, 3} runs over
+ * NVLink. Per level every partition stores its discoveries (top-down: its
+ * queue segment; bottom-up: its next-bitmap slice) straight into every
+ * peer's buffers, then one flag round (a sequence-numbered slot per
+ * partition in every partition's exchange block) replaces the allgather and
+ * the host round trip; every partition applies the reference's 5 % rule to
+ * the summed counts. Replaces, for several GPUs, what pbfs_graph + pbfs_bfs
+ * do for one (run_bfs, kernels.hpp:80-81). Hybrid (5 % rule) and its
+ * top-down-only dispatch. Peer access is enabled between distinct devices
+ * (PBFS_E_DEVICE if a pair has no peer path). */
+typedef struct pbfs_multi pbfs_multi;
+
+typedef struct pbfs_multi_info {
+  uint64_t vertex_count;
+  uint64_t edge_count;
+  uint64_t padded_count;      /* gid space */
+  uint64_t local_arcs[8];     /* per partition (row slice = column slice arcs) */
+  uint32_t partitions;
+  uint32_t devices;           /* distinct devices (= launches per traversal) */
+  uint32_t ctas_per_partition;
+  uint32_t relabel_hashed;
+} pbfs_multi_info;
+
+/* Uploads the host CSR once per device, builds each partition there. */
+pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices,
+                              uint32_t num_partitions, pbfs_multi** out);
+pbfs_status pbfs_multi_destroy(pbfs_multi* m);
+pbfs_status pbfs_multi_get_info(const pbfs_multi* m, pbfs_multi_info* info);
+/* Synchronous traversal: distances gathered in vertex order into dist_host
+ * (may be NULL), level records from partition 0, device_ms = first device's
+ * start to the last device's end. Same checks and errors as pbfs_bfs. */
+pbfs_status pbfs_multi_bfs(pbfs_multi* m, uint32_t source, const pbfs_config* cfg,
+                           uint32_t* dist_host, pbfs_level* levels, uint32_t levels_cap,
+                           pbfs_run_info* info);
+/* Enqueue-only traversal (one launch per device); pbfs_multi_sync waits for
+ * every device and reports the span (may be NULL) and any overflow. */
+pbfs_status pbfs_multi_bfs_async(pbfs_multi* m, uint32_t source, const pbfs_config* cfg);
+pbfs_status pbfs_multi_sync(pbfs_multi* m, float* device_ms);
+/* The first device's stream (cudaStream_t as void*): every traversal joins
+ * on it, so an event recorded there after pbfs_multi_bfs_async follows the
+ * traversal on every device. */
+pbfs_status pbfs_multi_stream(pbfs_multi* m, void** stream);
+/* Reached-component figures of the last traversal (summed over partitions). */
+pbfs_status pbfs_multi_component(pbfs_multi* m, uint64_t* n_reached, uint64_t* arcs_reached);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,12 @@ class PartInfo(ctypes.Structure):
                 ("reserved", c_u32), ("frontier", c_vp), ("next", c_vp), ("dist_local", c_vp)]
 
 
+class MultiInfo(ctypes.Structure):
+    _fields_ = [("vertex_count", c_u64), ("edge_count", c_u64), ("padded_count", c_u64),
+                ("local_arcs", c_u64 * 8), ("partitions", c_u32), ("devices", c_u32),
+                ("ctas_per_partition", c_u32), ("relabel_hashed", c_u32)]
+
+
 P = ctypes.POINTER
 
 # (name, restype, argtypes) for every symbol include/pbfs.h declares.
@@ -128,6 +134,14 @@ SIGNATURES = [
     ("pbfs_part_unrelabel", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("pbfs_part_copy_dist", ctypes.c_int, [c_vp, c_vp]),
     ("pbfs_part_unrelabel_host", ctypes.c_int, [c_vp, c_vp, c_vp]),
+    ("pbfs_multi_create", ctypes.c_int, [P(Csr), P(c_i32), c_u32, P(c_vp)]),
+    ("pbfs_multi_destroy", ctypes.c_int, [c_vp]),
+    ("pbfs_multi_get_info", ctypes.c_int, [c_vp, P(MultiInfo)]),
+    ("pbfs_multi_bfs", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp, P(Level), c_u32, P(RunInfo)]),
+    ("pbfs_multi_bfs_async", ctypes.c_int, [c_vp, c_u32, P(Config)]),
+    ("pbfs_multi_sync", ctypes.c_int, [c_vp, P(ctypes.c_float)]),
+    ("pbfs_multi_stream", ctypes.c_int, [c_vp, P(c_vp)]),
+    ("pbfs_multi_component", ctypes.c_int, [c_vp, P(c_u64), P(c_u64)]),
 ]
 
 

@@ -354,9 +354,17 @@ struct GridBarrier {
 };
 
 // Per-warp discovery buffer in shared memory (LocalFrontier analogue).
-struct WarpPush {
+// kPeers (the multi-partition engine, pbfs_multi.cu): a flush writes the
+// entries, offset by `lo` (local id -> global id), into `ndst` queue segments
+// -- this partition's segment in every partition's queue, peers' included --
+// so the frontier exchange rides on the level's own stores.
+template <bool kPeers>
+struct WarpPushT {
   uint32_t* buf;  // kPushBuf entries in smem
   int count;      // warp-uniform
+  uint32_t* const* dst = nullptr;  // kPeers: smem array of ndst segment bases
+  int ndst = 0;
+  uint32_t lo = 0;
   __device__ __forceinline__ void flush(uint32_t* out, unsigned long long* counter,
                                         unsigned long long cap, unsigned int* overflow) {
     __syncwarp();
@@ -365,7 +373,14 @@ struct WarpPush {
       if (lane_id() == 0) base = atomicAdd(counter, (unsigned long long)count);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base + count <= cap) {
-        for (int i = lane_id(); i < count; i += 32) out[base + i] = buf[i];
+        if constexpr (kPeers) {
+          for (int r = 0; r < ndst; ++r) {
+            uint32_t* o = dst[r] + base;
+            for (int i = lane_id(); i < count; i += 32) o[i] = buf[i] + lo;
+          }
+        } else {
+          for (int i = lane_id(); i < count; i += 32) out[base + i] = buf[i];
+        }
       } else if (lane_id() == 0) {
         atomicExch(overflow, 1u);
       }
@@ -409,6 +424,7 @@ struct WarpPush {
     count += k;
   }
 };
+using WarpPush = WarpPushT<false>;
 
 template <typename OffT>
 __device__ __forceinline__ unsigned long long degree_of(const Params<OffT>& p, uint32_t v) {
@@ -436,10 +452,10 @@ __device__ __forceinline__ uint32_t probe_word(const Params<OffT>& p, uint32_t v
 // in three stages so nothing waits on a single round trip: all K probe
 // loads, then all K claim atomics (results consumed only afterwards), then
 // the dist stores and queue appends. okm bit k marks a live edge slot.
-template <int C, int K, typename OffT>
+template <int C, int K, typename OffT, class WP>
 __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
                                             const uint32_t (&v)[K], uint32_t okm,
-                                            uint32_t* qout, WarpPush& wp, LevelCnt* cnt,
+                                            uint32_t* qout, WP& wp, LevelCnt* cnt,
                                             WarpTally& t, uint32_t* obm) {
   // Unconditional probes (dead slots hold a valid vertex id): predicated
   // loads end up in separate blocks that ptxas interleaves with their uses,
@@ -531,9 +547,9 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
 // Warp-cooperative expansion of up to 32 light vertices (lane i holds vertex
 // i's [beg, beg+deg)): inclusive shuffle scan of the degrees, then 4x32 edges
 // per step, each lane locating its owner by a 5-step shuffle binary search.
-template <int C, typename OffT>
+template <int C, typename OffT, class WP>
 __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t nd, OffT beg,
-                                               uint32_t deg, uint32_t* qout, WarpPush& wp,
+                                               uint32_t deg, uint32_t* qout, WP& wp,
                                                LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
   constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
@@ -576,9 +592,9 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
 
 // Static-first work distribution: warp gw takes slice gw first and only
 // then falls back to an atomic cursor, so a tiny frontier costs no atomics.
-template <int C, typename OffT>
-__device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint32_t* qin,
-                               unsigned long long qlen, uint32_t* qout, WarpPush& wp,
+template <int C, typename OffT, class QV = const uint32_t*, class WP = WarpPush>
+__device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, QV qin,
+                               unsigned long long qlen, uint32_t* qout, WP& wp,
                                LevelCnt* cnt, WarpTally& t, uint32_t* obm, uint32_t* stale,
                                VGrid vg = hw_grid()) {
   const unsigned FULL = 0xffffffffu;
@@ -651,9 +667,9 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, const uint
 // A hub's neighbours are dense in id space, so one probe instruction touches
 // ~2-3 distinct 128 B bitmap lines instead of ~32 -- the L1TEX line rate, not
 // DRAM, is what bounds a random-probe loop on this part.
-template <int C, typename OffT>
+template <int C, typename OffT, class WP = WarpPush>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
-                               uint32_t* qout, WarpPush& wp, LevelCnt* cnt, WarpTally& t,
+                               uint32_t* qout, WP& wp, LevelCnt* cnt, WarpTally& t,
                                uint32_t* obm, VGrid vg = hw_grid()) {
   constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
@@ -847,10 +863,18 @@ __device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const ui
 //     lane refill: a lane whose vertex is settled (parent found or list
 //     exhausted) takes the next miss, so the warp is not held to its longest
 //     scan (ER levels scan ~12 edges per vertex with a long geometric tail).
+// Optional copies of the `next` words a bottom-up level produces (the
+// multi-partition engine's peers' bitmaps at this partition's slice offset:
+// the exchange fused into the level, pbfs_multi.cu).
+struct NextPeers {
+  uint32_t* const* dst;  // shared memory, n entries
+  int n;
+};
+
 template <int GPT, typename OffT>
 __device__ void bu_phase_t(const Params<OffT>& p, uint32_t depth, const uint32_t* front,
                            uint32_t* next, uint32_t* list, uint32_t* found, WarpTally& t,
-                           unsigned int* cursor, VGrid vg) {
+                           unsigned int* cursor, VGrid vg, NextPeers peers = NextPeers{nullptr, 0}) {
   constexpr bool sparse = GPT > 1;
   constexpr int KB = kBuSlots;
   const unsigned FULL = 0xffffffffu;
@@ -889,11 +913,16 @@ __device__ void bu_phase_t(const Params<OffT>& p, uint32_t depth, const uint32_t
     const uint32_t total = __shfl_sync(FULL, incl, 31);
     if (total == 0 || sparse) {
       // Sparse tasks mark discoveries straight into next / visited (global
-      // atomics; there are few), so their next words start zeroed.
+      // atomics; there are few), so their next words start zeroed. (The
+      // multi-partition engine never runs sparse tasks: its peers' copies
+      // are plain stores of whole words.)
 #pragma unroll
       for (int j = 0; j < GPT; ++j) {
         const uint32_t w = wbase + j * 32 + lane;
-        if (w < p.words) next[w] = 0;
+        if (w < p.words) {
+          next[w] = 0;
+          for (int r = 0; r < peers.n; ++r) peers.dst[r][w] = 0;
+        }
       }
       if (total == 0) {
         task = __shfl_sync(FULL, nxt, 0);
@@ -1052,6 +1081,7 @@ __device__ void bu_phase_t(const Params<OffT>& p, uint32_t depth, const uint32_t
     if (!sparse && wbase + lane < p.words) {
       const uint32_t f = found[lane];
       next[wbase + lane] = f;
+      for (int r = 0; r < peers.n; ++r) peers.dst[r][wbase + lane] = f;
       if (f) p.visited[wbase + lane] = visw[0] | f;
     }
     task = __shfl_sync(FULL, nxt, 0);
@@ -1062,11 +1092,12 @@ template <typename OffT>
 __device__ __forceinline__ void bu_phase(const Params<OffT>& p, uint32_t depth,
                                          const uint32_t* front, uint32_t* next, uint32_t* list,
                                          uint32_t* found, WarpTally& t, unsigned int* cursor,
-                                         bool sparse, VGrid vg = hw_grid()) {
+                                         bool sparse, VGrid vg = hw_grid(),
+                                         NextPeers peers = NextPeers{nullptr, 0}) {
   if (sparse) {
     bu_phase_t<kBuSparseGroups>(p, depth, front, next, list, found, t, cursor, vg);
   } else {
-    bu_phase_t<1>(p, depth, front, next, list, found, t, cursor, vg);
+    bu_phase_t<1>(p, depth, front, next, list, found, t, cursor, vg, peers);
   }
 }
 

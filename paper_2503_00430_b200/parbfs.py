@@ -237,6 +237,12 @@ class CsrGraph:
             g.close()
         self._device.clear()
 
+    def multi_device(self, devices) -> "MultiDeviceGraph":
+        """The graph partitioned over `devices` (one partition per entry;
+        repeats = several partitions on one GPU) for the multi-partition
+        engine (pbfs_multi_create)."""
+        return MultiDeviceGraph(self, devices)
+
 
 def _from_host_handle(h: ctypes.c_void_p) -> CsrGraph:
     view = L.Csr()
@@ -498,6 +504,80 @@ class BfsResult:
 
 
 # ---- device graph + traversal -------------------------------------------------------
+class MultiDeviceGraph:
+    """pbfs_multi: the 1D vertex partition with the frontier exchange fused
+    into one persistent launch per device (see include/pbfs.h)."""
+
+    def __init__(self, graph: "CsrGraph", devices):
+        devs = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        v = graph._view()
+        h = ctypes.c_void_p()
+        _check(lib.pbfs_multi_create(ctypes.byref(v), devs, len(devices), ctypes.byref(h)))
+        self.h = h
+        self.vertex_count = graph.vertex_count
+        self.devices = list(devices)
+        i = L.MultiInfo()
+        _check(lib.pbfs_multi_get_info(h, ctypes.byref(i)))
+        self.info = {k: (list(getattr(i, k)) if k == "local_arcs" else getattr(i, k))
+                     for k, _ in L.MultiInfo._fields_}
+        self.info["local_arcs"] = self.info["local_arcs"][:len(devices)]
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib.pbfs_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bfs(self, source: int, config: KernelConfig, want_distances: bool = True,
+            want_trace: bool = True, out: Optional[np.ndarray] = None) -> BfsResult:
+        c = config._c()
+        dist = None
+        if want_distances:
+            dist = out if out is not None else np.empty(self.vertex_count, dtype=np.uint32)
+        cap = min(self.vertex_count + 1, 1 << 16) if want_trace else 0
+        levels = (L.Level * cap)() if cap else None
+        info = L.RunInfo()
+        t0 = time.perf_counter_ns()
+        _check(lib.pbfs_multi_bfs(self.h, int(source) & 0xFFFFFFFF, ctypes.byref(c),
+                                  dist.ctypes.data if dist is not None else None, levels, cap,
+                                  ctypes.byref(info)))
+        t1 = time.perf_counter_ns()
+        trace = TraversalTrace(variant=KernelVariant(config.variant),
+                               worker_count=config.worker_count, source=int(source),
+                               total_elapsed_ns=t1 - t0, device_ms=float(info.device_ms))
+        for i in range(min(info.levels, cap)):
+            r = levels[i]
+            trace.records.append(LevelRecord(r.depth, TraversalPhase(r.phase), r.frontier_size,
+                                             r.distinct_size, r.duplicate_count,
+                                             r.edges_examined, r.flush_events, r.elapsed_ns))
+        return BfsResult(dist, trace)
+
+    def bfs_async(self, source: int, config: KernelConfig) -> None:
+        c = config._c()
+        _check(lib.pbfs_multi_bfs_async(self.h, int(source) & 0xFFFFFFFF, ctypes.byref(c)))
+
+    def sync(self) -> float:
+        ms = ctypes.c_float()
+        _check(lib.pbfs_multi_sync(self.h, ctypes.byref(ms)))
+        return ms.value
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _check(lib.pbfs_multi_stream(self.h, ctypes.byref(s)))
+        return s.value or 0
+
+    def component(self):
+        nr = ctypes.c_uint64()
+        ar = ctypes.c_uint64()
+        _check(lib.pbfs_multi_component(self.h, ctypes.byref(nr), ctypes.byref(ar)))
+        return nr.value, ar.value
+
+
 class DeviceGraph:
     """A graph resident in HBM (pbfs_graph handle) with its traversal scratch."""
 
