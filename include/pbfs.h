@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define PBFS_ABI_VERSION 1u
+#define PBFS_ABI_VERSION 2u
 #define PBFS_UNREACHED 0xFFFFFFFFu /* == parbfs::kUnreached (types.hpp:19) == int32 -1 */
 
 typedef enum pbfs_status {
@@ -112,6 +112,16 @@ typedef struct pbfs_run_info {
 typedef struct pbfs_graph_options {
   int32_t device;               /* CUDA ordinal */
   uint32_t device_offset_bytes; /* 0 = auto (4 if edge_count < 2^31 else 8), 4 or 8 */
+  /* Optional multi-GPU placement (SURVEY.md §8(b) "devices[], num_devices"):
+   * with num_devices > 1 the handle partitions the graph over devices[0..n)
+   * (one partition each; repeats place several partitions on one GPU) and
+   * every traversal entry point runs the multi-partition engine
+   * (pbfs_multi_*, below) -- so run_bfs / a KernelFn built on this handle
+   * reach every GPU. num_devices <= 1 (or devices == NULL): one GPU,
+   * `device`. */
+  const int32_t* devices;
+  uint32_t num_devices;
+  uint32_t reserved;
 } pbfs_graph_options;
 
 typedef struct pbfs_graph_info {
@@ -124,7 +134,7 @@ typedef struct pbfs_graph_info {
   int32_t device;
   uint32_t grid_blocks; /* persistent traversal grid (SMs x resident CTAs) */
   uint32_t block_threads;
-  uint32_t reserved;
+  uint32_t partitions;  /* 1, or the multi-GPU placement's partition count */
 } pbfs_graph_info;
 
 typedef struct pbfs_graph pbfs_graph;
@@ -398,6 +408,11 @@ pbfs_status pbfs_multi_sync(pbfs_multi* m, float* device_ms);
 pbfs_status pbfs_multi_stream(pbfs_multi* m, void** stream);
 /* Reached-component figures of the last traversal (summed over partitions). */
 pbfs_status pbfs_multi_component(pbfs_multi* m, uint64_t* n_reached, uint64_t* arcs_reached);
+/* Makes `stream` (a cudaStream_t on any device) wait for the last traversal. */
+pbfs_status pbfs_multi_join(pbfs_multi* m, void* stream);
+/* Level records of the last traversal (partition 0's), as pbfs_graph_trace. */
+pbfs_status pbfs_multi_trace(pbfs_multi* m, pbfs_level* levels, uint32_t levels_cap,
+                             uint32_t* count);
 
 #ifdef __cplusplus
 }

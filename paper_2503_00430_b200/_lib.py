@@ -47,14 +47,15 @@ class RunInfo(ctypes.Structure):
 
 
 class GraphOptions(ctypes.Structure):
-    _fields_ = [("device", c_i32), ("device_offset_bytes", c_u32)]
+    _fields_ = [("device", c_i32), ("device_offset_bytes", c_u32), ("devices", c_vp),
+                ("num_devices", c_u32), ("reserved", c_u32)]
 
 
 class GraphInfo(ctypes.Structure):
     _fields_ = [("vertex_count", c_u64), ("edge_count", c_u64), ("max_degree", c_u64),
                 ("device_bytes", c_u64), ("device_offset_bytes", c_u32), ("symmetric", c_u32),
                 ("device", c_i32), ("grid_blocks", c_u32), ("block_threads", c_u32),
-                ("reserved", c_u32)]
+                ("partitions", c_u32)]
 
 
 class GenSpec(ctypes.Structure):
@@ -142,6 +143,8 @@ SIGNATURES = [
     ("pbfs_multi_sync", ctypes.c_int, [c_vp, P(ctypes.c_float)]),
     ("pbfs_multi_stream", ctypes.c_int, [c_vp, P(c_vp)]),
     ("pbfs_multi_component", ctypes.c_int, [c_vp, P(c_u64), P(c_u64)]),
+    ("pbfs_multi_join", ctypes.c_int, [c_vp, c_vp]),
+    ("pbfs_multi_trace", ctypes.c_int, [c_vp, P(Level), c_u32, P(c_u32)]),
 ]
 
 

@@ -194,6 +194,9 @@ class Widener {
 
 struct pbfs_graph {
   std::mutex mu;
+  // Multi-GPU placement (pbfs_graph_options.devices): every traversal entry
+  // point forwards to the multi-partition engine (pbfs_multi.cu).
+  pbfs_multi* multi = nullptr;
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -275,6 +278,11 @@ pbfs_status dalloc(pbfs_graph* g, T** p, size_t bytes) {
 
 void release(pbfs_graph* g) {
   if (!g) return;
+  if (g->multi) {
+    pbfs_multi_destroy(g->multi);
+    delete g;
+    return;
+  }
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(g->device);
@@ -554,6 +562,24 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
   g->m = m;
   g->offb = offb;
   g->symmetric = csr->symmetric != 0;
+  if (opt && opt->devices && opt->num_devices > 1) {
+    // Partitioned over several devices: the handle is a pbfs_multi.
+    g->device = opt->devices[0];
+    g->offb = 8;
+    for (uint64_t v = 0; v < n; ++v) {
+      g->max_degree = std::max<uint64_t>(g->max_degree, csr_offset(csr, v + 1) - csr_offset(csr, v));
+    }
+    st = pbfs_multi_create(csr, opt->devices, opt->num_devices, &g->multi);
+    if (st != PBFS_OK) {
+      delete g;
+      return st;
+    }
+    pbfs_multi_info mi;
+    pbfs_multi_get_info(g->multi, &mi);
+    g->grid = static_cast<int>(mi.ctas_per_partition * mi.partitions);
+    *out = g;
+    return PBFS_OK;
+  }
   // Host-side per-graph facts: max degree, heavy-item capacity, the
   // zero-degree mask that lets bottom-up skip isolated vertices.
   // Whole 32-word groups: bottom-up takes 16-word groups, the merge and
@@ -760,6 +786,13 @@ pbfs_status pbfs_graph_get_info(const pbfs_graph* g, pbfs_graph_info* info) {
   info->device = g->device;
   info->grid_blocks = static_cast<uint32_t>(g->grid);
   info->block_threads = kThreads;
+  if (g->multi) {
+    pbfs_multi_info mi;
+    pbfs_multi_get_info(g->multi, &mi);
+    info->partitions = mi.partitions;
+  } else {
+    info->partitions = 1;
+  }
   return PBFS_OK;
 }
 
@@ -835,6 +868,7 @@ extern "C" {
 pbfs_status pbfs_bfs(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, uint32_t* dist_host,
                      pbfs_level* levels, uint32_t levels_cap, pbfs_run_info* info) {
   if (!g) return fail(PBFS_E_INPUT, "null graph");
+  if (g->multi) return pbfs_multi_bfs(g->multi, source, cfg, dist_host, levels, levels_cap, info);
   std::lock_guard<std::mutex> lock(g->mu);
   return pbfs_bfs_locked(g, source, cfg, dist_host, levels, levels_cap, info);
 }
@@ -844,6 +878,15 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
                            pbfs_run_info* infos) {
   if (!g) return fail(PBFS_E_INPUT, "null graph");
   if (count && (!sources || !dist_host)) return fail(PBFS_E_INPUT, "null argument");
+  if (g->multi) {
+    for (uint32_t i = 0; i < count; ++i) {
+      pbfs_status st = pbfs_multi_bfs(g->multi, sources[i], cfg, dist_host[i], nullptr, 0,
+                                      infos ? &infos[i] : nullptr);
+      if (st != PBFS_OK) return st;
+      if (infos) infos[i].transfer_width = 4;
+    }
+    return PBFS_OK;
+  }
   std::lock_guard<std::mutex> lock(g->mu);
   Launch l;
   for (uint32_t i = 0; i < count; ++i) {
@@ -1005,6 +1048,13 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
 
 pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, void* stream) {
   if (!g) return fail(PBFS_E_INPUT, "null graph");
+  if (g->multi) {
+    // The launches go to the engine's own per-device streams; the caller's
+    // stream then waits for the traversal on every device.
+    pbfs_status st = pbfs_multi_bfs_async(g->multi, source, cfg);
+    if (st != PBFS_OK || !stream) return st;
+    return pbfs_multi_join(g->multi, stream);
+  }
   std::lock_guard<std::mutex> lock(g->mu);
   Launch l;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
@@ -1020,6 +1070,7 @@ pbfs_status pbfs_bfs_async(pbfs_graph* g, uint32_t source, const pbfs_config* cf
 
 pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream) {
   if (!g) return fail(PBFS_E_INPUT, "null graph");
+  if (g->multi) return pbfs_multi_sync(g->multi, nullptr);
   std::lock_guard<std::mutex> lock(g->mu);
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->stream;
@@ -1045,6 +1096,7 @@ pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offse
   if (!g || !row_offsets || !column_indices || !offset_bytes) {
     return fail(PBFS_E_INPUT, "null argument");
   }
+  if (g->multi) return fail(PBFS_E_CONFIG, "a multi-device handle holds partitions, not the full CSR");
   *row_offsets = g->rowptr;
   *column_indices = g->col;
   *offset_bytes = g->offb;
@@ -1054,6 +1106,7 @@ pbfs_status pbfs_graph_device_arrays(const pbfs_graph* g, const void** row_offse
 pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_cap,
                              uint32_t* count) {
   if (!g || !count || (levels_cap && !levels)) return fail(PBFS_E_INPUT, "null argument");
+  if (g->multi) return pbfs_multi_trace(g->multi, levels, levels_cap, count);
   std::lock_guard<std::mutex> lock(g->mu);
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
   PBFS_CUDA(cudaEventSynchronize(g->order_ev), "traversal");
@@ -1073,12 +1126,17 @@ pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_
 
 pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev) {
   if (!g || !dist_dev) return fail(PBFS_E_INPUT, "null argument");
+  if (g->multi) {
+    return fail(PBFS_E_CONFIG, "a multi-device handle keeps distances in its partitions: "
+                               "read them with pbfs_bfs (dist_host)");
+  }
   *dist_dev = g->dist;
   return PBFS_OK;
 }
 
 pbfs_status pbfs_graph_component(pbfs_graph* g, uint64_t* n_reached, uint64_t* arcs_reached) {
   if (!g || !n_reached || !arcs_reached) return fail(PBFS_E_INPUT, "null argument");
+  if (g->multi) return pbfs_multi_component(g->multi, n_reached, arcs_reached);
   std::lock_guard<std::mutex> lock(g->mu);
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
   pbfs_status st = order_after_last(g, g->stream);

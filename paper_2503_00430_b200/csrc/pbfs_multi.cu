@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -120,19 +121,38 @@ struct SegQueue {
   }
 };
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Memory-model scope of the exchange: system scope when partitions sit on
+// different GPUs (peer stores over NVLink), GPU scope when every partition
+// shares one device (loopback), where the partition barrier's own
+// release/acquire already covers the peer stores.
+template <bool kSys>
+__device__ __forceinline__ void st_relaxed_x(unsigned long long* p, unsigned long long v) {
+  if constexpr (kSys) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  } else {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  }
 }
-__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+template <bool kSys>
+__device__ __forceinline__ unsigned long long ld_relaxed_x(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if constexpr (kSys) {
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  } else {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  }
   return v;
 }
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+template <bool kSys>
+__device__ __forceinline__ void fence_x() {
+  if constexpr (kSys) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  } else {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+}
 
+template <bool kSys>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_multi(MultiParams mp) {
   __shared__ __align__(16) uint32_t s_list[kWarps][kListCap];
   __shared__ uint32_t s_found[kWarps][kGroupWords];
@@ -199,43 +219,49 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_multi(MultiParams mp
   bar.sync();
 
   // One exchange: publish (a, b), wait for every partition's, leave the P
-  // pairs in s_x. Callers have released their peer stores (fence_sys) and
-  // passed the partition barrier first.
+  // pairs in s_x. Callers have released their peer stores (release_cta) and
+  // passed the partition barrier first. One fence per side: the writer
+  // stores every value, fences, then every sequence number; a reader polls
+  // the sequence numbers, fences, then reads the values.
   auto exchange = [&](unsigned long long a, unsigned long long b) {
     const unsigned long long seq = ((unsigned long long)mp.run << 32) | (xstep + 1);
     const int par = xstep & 1;
     if (vg.cta == 0 && threadIdx.x == 0) {
       for (uint32_t r = 0; r < P; ++r) {
         XSlot* sl = &D->peer_x[r]->slot[par][me];
-        st_relaxed_sys(&sl->produced, a);
-        st_relaxed_sys(&sl->edges, b);
-        st_release_sys(&sl->seq, seq);
+        st_relaxed_x<kSys>(&sl->produced, a);
+        st_relaxed_x<kSys>(&sl->edges, b);
       }
+      fence_x<kSys>();
+      for (uint32_t r = 0; r < P; ++r) st_relaxed_x<kSys>(&D->peer_x[r]->slot[par][me].seq, seq);
     }
     if (threadIdx.x == 0) {
       Xchg* x = D->peer_x[me];
       const unsigned long long t0 = globaltimer();
       for (uint32_t r = 0; r < P; ++r) {
-        while (ld_relaxed_sys(&x->slot[par][r].seq) != seq) {
+        while (ld_relaxed_x<kSys>(&x->slot[par][r].seq) != seq) {
           // A partition that never arrives (a peer launch that failed to
           // start) must not wedge the device: abort the launch after 30 s.
           if (globaltimer() - t0 > 30000000000ull) __trap();
         }
       }
-      fence_sys();
+      fence_x<kSys>();
       for (uint32_t r = 0; r < P; ++r) {
-        s_x[r][0] = ld_relaxed_sys(&x->slot[par][r].produced);
-        s_x[r][1] = ld_relaxed_sys(&x->slot[par][r].edges);
+        s_x[r][0] = ld_relaxed_x<kSys>(&x->slot[par][r].produced);
+        s_x[r][1] = ld_relaxed_x<kSys>(&x->slot[par][r].edges);
       }
     }
     ++xstep;
     __syncthreads();
   };
-  // Every CTA's stores to other partitions' memory, made visible system-wide
-  // before the partition barrier that precedes an exchange.
+  // Every CTA's stores to other GPUs' memory, made visible system-wide
+  // before the partition barrier that precedes an exchange (on one GPU the
+  // barrier's release/acquire at GPU scope covers them).
   auto release_cta = [&]() {
-    __syncthreads();
-    if (threadIdx.x == 0) fence_sys();
+    if constexpr (kSys) {
+      __syncthreads();
+      if (threadIdx.x == 0) fence_x<true>();
+    }
   };
 
   uint32_t depth = 0;
@@ -363,6 +389,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_multi(MultiParams mp
   }
 }
 
+// Hub items of the column slice when a small frontier splits hubs into
+// 2^kSmallChunkLog2-edge items (td_phase_light), for hubs above heavy_deg.
+__global__ void k_small_items(const unsigned long long* __restrict__ colptr, uint64_t npad,
+                              uint32_t heavy_deg, unsigned long long* items) {
+  unsigned long long c = 0;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < npad;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = colptr[u + 1] - colptr[u];
+    if (d > heavy_deg) c += (d + (1ull << kSmallChunkLog2) - 1) >> kSmallChunkLog2;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(items, c);
+}
+
 __global__ void k_unrelabel_gather(const uint32_t* __restrict__ dist_pi, uint64_t n,
                                    const uint32_t* __restrict__ gid, uint32_t* dist) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
@@ -391,6 +432,12 @@ struct pbfs_multi {
   struct Group {
     int device = 0;
     uint32_t first = 0, count = 0, ctas_per_part = 0;
+    // visited | bm[0] | bm[1] of every partition of this device in ONE block,
+    // under the launch's persisting-L2 window (the probe working set must not
+    // be evicted by the multi-GB column stream, as in the single-GPU engine).
+    uint32_t* bitmaps = nullptr;
+    size_t bitmap_bytes = 0;
+    size_t persist = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t start = nullptr, end = nullptr;
     PartDev* parts_dev = nullptr;  // this device's copy of the descriptor array
@@ -403,6 +450,10 @@ struct pbfs_multi {
   uint64_t npad = 0;
   uint32_t run = 0;
   bool launched = false;
+  // System-scope exchange: partitions span several GPUs, or
+  // PBFS_MULTI_SYS_SCOPE=1 (test hook: the multi-GPU memory-model path on
+  // one GPU).
+  bool sys = false;
   pbfs_config last_cfg{};
 };
 
@@ -423,6 +474,7 @@ void multi_release(pbfs_multi* m) {
   for (auto& g : m->groups) {
     cudaSetDevice(g.device);
     if (g.parts_dev) cudaFree(g.parts_dev);
+    if (g.bitmaps) cudaFree(g.bitmaps);
     if (g.start) cudaEventDestroy(g.start);
     if (g.end) cudaEventDestroy(g.end);
     if (g.stream) cudaStreamDestroy(g.stream);
@@ -567,40 +619,6 @@ pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices, uint3
     if ((st = malloc_on(m, i, &m->xchg[i], sizeof(Xchg))) != PBFS_OK) return bail(st);
     MCUDA(cudaMemset(m->xchg[i], 0, sizeof(Xchg)), "memset exchange block");
   }
-  // Descriptors (identical bytes on every device: unified addressing).
-  std::vector<PartDev> desc(num_partitions);
-  for (uint32_t i = 0; i < num_partitions; ++i) {
-    pbfs_part* g = m->parts[i];
-    PartDev& d = desc[i];
-    std::memset(&d, 0, sizeof(d));
-    d.td = pbfs::part::td_params(g);
-    d.bu = pbfs::part::bu_params(g);
-    d.td.qcap = m->seg_cap;
-    d.bm[0] = g->bm[0];
-    d.bm[1] = g->bm[1];
-    d.q[0] = m->q[0][i];
-    d.q[1] = m->q[1][i];
-    for (uint32_t r = 0; r < num_partitions; ++r) {
-      d.peer_bm[r][0] = m->parts[r]->bm[0];
-      d.peer_bm[r][1] = m->parts[r]->bm[1];
-      d.peer_q[r][0] = m->q[0][r];
-      d.peer_q[r][1] = m->q[1][r];
-      d.peer_x[r] = m->xchg[r];
-    }
-    d.ctl = g->ctl;
-    d.recs = g->recs;
-    d.rec_cap = pbfs::part::kPartRecCap;
-    d.mask = g->mask;
-    d.dist = g->dist;
-    d.visited = g->visited;
-    d.lo = g->lo;
-    d.nloc = g->nloc;
-    d.lwords = g->lwords;
-    d.words_total = g->words_total;
-    d.seg_cap = m->seg_cap;
-    d.col_maxdeg = g->col_maxdeg;
-    d.rank = i;
-  }
   // Launch groups: one per distinct device, partitions of a device contiguous.
   for (uint32_t i = 0; i < num_partitions;) {
     uint32_t j = i;
@@ -618,6 +636,104 @@ pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices, uint3
     m->groups.push_back(grp);
     i = j;
   }
+  // Descriptors (identical bytes on every device: unified addressing).
+  // Per device: one block of every local partition's visited | bm[0] | bm[1].
+  std::vector<uint32_t*> vis(num_partitions), bm0(num_partitions), bm1(num_partitions);
+  for (auto& grp : m->groups) {
+    MCUDA(cudaSetDevice(grp.device), "cudaSetDevice");
+    size_t words = 0;
+    for (uint32_t i = grp.first; i < grp.first + grp.count; ++i) {
+      words += m->parts[i]->lwords + 2 * m->parts[i]->words_total;
+    }
+    grp.bitmap_bytes = words * 4;
+    MCUDA(cudaMalloc(&grp.bitmaps, grp.bitmap_bytes), "bitmap block");
+    uint32_t* at = grp.bitmaps;
+    for (uint32_t i = grp.first; i < grp.first + grp.count; ++i) {
+      vis[i] = at;
+      at += m->parts[i]->lwords;
+      bm0[i] = at;
+      at += m->parts[i]->words_total;
+      bm1[i] = at;
+      at += m->parts[i]->words_total;
+    }
+    cudaDeviceProp prop;
+    MCUDA(cudaGetDeviceProperties(&prop, grp.device), "props");
+    if (prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0) {
+      grp.bitmap_bytes = std::min<size_t>(grp.bitmap_bytes, prop.accessPolicyMaxWindowSize);
+      const size_t want = std::min<size_t>(grp.bitmap_bytes, prop.persistingL2CacheMaxSize);
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur >= want || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+        grp.persist = std::max(cur, want);
+      }
+      cudaGetLastError();
+    }
+  }
+  // Top-down hub items: the partition's own capacity, or the small-frontier
+  // split's (2^kSmallChunkLog2-edge items) if larger; graphs of >= 2^30
+  // local arcs take the single-GPU engine's big split.
+  std::vector<HeavyItem*> heavy(num_partitions);
+  std::vector<unsigned long long> heavy_cap(num_partitions);
+  for (uint32_t i = 0; i < num_partitions; ++i) {
+    pbfs_part* g = m->parts[i];
+    MCUDA(cudaSetDevice(g->device), "cudaSetDevice");
+    unsigned long long* cnt = nullptr;
+    if ((st = malloc_on(m, i, &cnt, 8)) != PBFS_OK) return bail(st);
+    MCUDA(cudaMemset(cnt, 0, 8), "memset");
+    k_small_items<<<1184, 256>>>(g->colptr, g->npad, kHeavyDeg, cnt);
+    unsigned long long small = 0;
+    MCUDA(cudaMemcpy(&small, cnt, 8, cudaMemcpyDeviceToHost), "small items");
+    heavy_cap[i] = std::max<unsigned long long>(g->heavy_cap, small);
+    if ((st = malloc_on(m, i, &heavy[i], std::max<unsigned long long>(heavy_cap[i], 1) *
+                                              sizeof(HeavyItem))) != PBFS_OK) {
+      return bail(st);
+    }
+  }
+  std::vector<PartDev> desc(num_partitions);
+  for (uint32_t i = 0; i < num_partitions; ++i) {
+    pbfs_part* g = m->parts[i];
+    PartDev& d = desc[i];
+    std::memset(&d, 0, sizeof(d));
+    d.td = pbfs::part::td_params(g);
+    d.bu = pbfs::part::bu_params(g);
+    d.td.qcap = m->seg_cap;
+    d.td.visited = d.bu.visited = vis[i];
+    d.td.heavy = heavy[i];
+    d.td.heavy_cap = heavy_cap[i];
+    d.td.small_chunks = 1;
+    if (g->m_loc >= kBigArcs) {
+      d.td.heavy_deg = kHeavyDegBig;
+      d.td.chunk_log2 = __builtin_ctz(kChunkBig);
+    }
+    d.bm[0] = bm0[i];
+    d.bm[1] = bm1[i];
+    d.q[0] = m->q[0][i];
+    d.q[1] = m->q[1][i];
+    for (uint32_t r = 0; r < num_partitions; ++r) {
+      d.peer_bm[r][0] = bm0[r];
+      d.peer_bm[r][1] = bm1[r];
+      d.peer_q[r][0] = m->q[0][r];
+      d.peer_q[r][1] = m->q[1][r];
+      d.peer_x[r] = m->xchg[r];
+    }
+    d.ctl = g->ctl;
+    d.recs = g->recs;
+    d.rec_cap = pbfs::part::kPartRecCap;
+    d.mask = g->mask;
+    d.dist = g->dist;
+    d.visited = vis[i];
+    d.lo = g->lo;
+    d.nloc = g->nloc;
+    d.lwords = g->lwords;
+    d.words_total = g->words_total;
+    d.seg_cap = m->seg_cap;
+    d.col_maxdeg = g->col_maxdeg;
+    d.rank = i;
+  }
+  {
+    const char* fs = std::getenv("PBFS_MULTI_SYS_SCOPE");
+    m->sys = m->groups.size() > 1 || (fs && fs[0] == '1');
+  }
   for (auto& grp : m->groups) {
     MCUDA(cudaSetDevice(grp.device), "cudaSetDevice");
     MCUDA(cudaStreamCreateWithFlags(&grp.stream, cudaStreamNonBlocking), "stream");
@@ -628,9 +744,12 @@ pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices, uint3
                      cudaMemcpyHostToDevice), "descriptors");
     cudaDeviceProp prop;
     MCUDA(cudaGetDeviceProperties(&prop, grp.device), "props");
-    cudaFuncSetAttribute(bfs_multi, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
+    const bool sys = m->sys;
+    const void* fn = sys ? reinterpret_cast<const void*>(&bfs_multi<true>)
+                         : reinterpret_cast<const void*>(&bfs_multi<false>);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 25);
     int occ = 0;
-    MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_multi, kThreads, 0), "occupancy");
+    MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0), "occupancy");
     if (occ < 1) return bail(fail(PBFS_E_DEVICE, "multi-partition kernel cannot be resident"));
     const uint32_t grid = static_cast<uint32_t>(prop.multiProcessorCount * occ);
     grp.ctas_per_part = grid / grp.count;
@@ -712,12 +831,25 @@ pbfs_status pbfs_multi_bfs_async(pbfs_multi* m, uint32_t source, const pbfs_conf
     lc.gridDim = dim3(grp.count * grp.ctas_per_part);
     lc.blockDim = dim3(kThreads);
     lc.stream = grp.stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    int nattr = 1;
+    if (grp.persist) {
+      attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[1].val.accessPolicyWindow.base_ptr = grp.bitmaps;
+      attr[1].val.accessPolicyWindow.num_bytes = grp.bitmap_bytes;
+      attr[1].val.accessPolicyWindow.hitRatio =
+          std::min(1.0f, static_cast<float>(grp.persist) / static_cast<float>(grp.bitmap_bytes));
+      attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      nattr = 2;
+    }
     lc.attrs = attr;
-    lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&lc, bfs_multi, mp);
+    lc.numAttrs = nattr;
+    // System-scope exchange only when the partitions span several GPUs.
+    cudaError_t e = m->sys ? cudaLaunchKernelEx(&lc, bfs_multi<true>, mp)
+                           : cudaLaunchKernelEx(&lc, bfs_multi<false>, mp);
     if (e != cudaSuccess) {
       cudaSetDevice(prev);
       return cuda_fail_m(e, "multi-partition traversal launch");
@@ -809,6 +941,36 @@ pbfs_status pbfs_multi_bfs(pbfs_multi* m, uint32_t source, const pbfs_config* cf
   cudaSetDevice(prev);
   if (levels && ctl.levels > pbfs::part::kPartRecCap) {
     return fail(PBFS_E_CAPACITY, "traversal depth exceeds the partitioned trace capacity");
+  }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_multi_join(pbfs_multi* m, void* stream) {
+  if (!m || !stream) return fail(PBFS_E_INPUT, "null argument");
+  std::lock_guard<std::mutex> lock(m->mu);
+  if (!m->launched) return PBFS_OK;
+  MCUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), m->all_done, 0), "join");
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_multi_trace(pbfs_multi* m, pbfs_level* levels, uint32_t levels_cap,
+                             uint32_t* count) {
+  if (!m || !count || (levels_cap && !levels)) return fail(PBFS_E_INPUT, "null argument");
+  pbfs_status st = pbfs_multi_sync(m, nullptr);
+  if (st != PBFS_OK) return st;
+  std::lock_guard<std::mutex> lock(m->mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  pbfs_part* p0 = m->parts[0];
+  MCUDA(cudaSetDevice(p0->device), "cudaSetDevice");
+  unsigned int nlev = 0;
+  MCUDA(cudaMemcpy(&nlev, &p0->ctl->levels, sizeof(nlev), cudaMemcpyDeviceToHost), "read control");
+  const uint32_t k = std::min<uint32_t>(std::min<uint32_t>(nlev, pbfs::part::kPartRecCap), levels_cap);
+  if (k) MCUDA(cudaMemcpy(levels, p0->recs, k * sizeof(pbfs_level), cudaMemcpyDeviceToHost), "read trace");
+  *count = k;
+  cudaSetDevice(prev);
+  if (nlev > pbfs::part::kPartRecCap) {
+    return fail(PBFS_E_CAPACITY, "the last traversal was deeper than the partitioned trace buffer");
   }
   return PBFS_OK;
 }

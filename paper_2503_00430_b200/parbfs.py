@@ -223,9 +223,12 @@ class CsrGraph:
         c.symmetric = int(self.symmetric)
         return c
 
-    def device(self, device: int = 0, offset_bytes: int = 0) -> "DeviceGraph":
-        """The resident device copy (created once per graph/device/offset width)."""
-        key = (device, offset_bytes)
+    def device(self, device=0, offset_bytes: int = 0) -> "DeviceGraph":
+        """The resident device copy (created once per graph/device/offset
+        width). `device` may be a list of CUDA ordinals: the graph is then
+        partitioned over them (pbfs_graph_options.devices, the
+        multi-partition engine) behind the same DeviceGraph interface."""
+        key = (tuple(device) if isinstance(device, (list, tuple)) else device, offset_bytes)
         g = self._device.get(key)
         if g is None:
             g = DeviceGraph(self, device=device, offset_bytes=offset_bytes)
@@ -581,9 +584,16 @@ class MultiDeviceGraph:
 class DeviceGraph:
     """A graph resident in HBM (pbfs_graph handle) with its traversal scratch."""
 
-    def __init__(self, graph: CsrGraph, device: int = 0, offset_bytes: int = 0):
+    def __init__(self, graph: CsrGraph, device=0, offset_bytes: int = 0):
         opt = L.GraphOptions()
-        opt.device = int(device)
+        if isinstance(device, (list, tuple)):
+            devs = (ctypes.c_int32 * len(device))(*[int(d) for d in device])
+            self._devs = devs
+            opt.device = int(device[0])
+            opt.devices = ctypes.cast(devs, ctypes.c_void_p)
+            opt.num_devices = len(device)
+        else:
+            opt.device = int(device)
         opt.device_offset_bytes = int(offset_bytes)
         v = graph._view()
         h = ctypes.c_void_p()
@@ -776,8 +786,10 @@ def bfs_topdown_periodic_flush(graph: CsrGraph, source: int, config: KernelConfi
 
 
 def run_bfs(graph: CsrGraph, source: int, config: KernelConfig, stats: GraphStats,
-            device: int = 0) -> BfsResult:
-    """kernels.cpp:657-691: large-diameter graphs run top-down only."""
+            device=0) -> BfsResult:
+    """kernels.cpp:657-691: large-diameter graphs run top-down only.
+    `device` may be a list of CUDA ordinals (the graph partitioned over
+    them, the multi-partition engine)."""
     effective = KernelConfig(**config.__dict__)
     if stats.category == GraphCategory.LargeDiameter:
         effective.force_top_down_only = True

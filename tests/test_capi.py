@@ -48,7 +48,7 @@ def test_struct_layout_matches_header(tmp_path):
 
 
 def test_abi_version_and_status_strings():
-    assert L.lib.pbfs_abi_version() == 1
+    assert L.lib.pbfs_abi_version() == 2
     assert L.lib.pbfs_status_string(0) == b"ok"
     assert L.lib.pbfs_status_string(4) == b"capacity error"
 

@@ -34,7 +34,11 @@ def check(port, g, mg, srcs, cfg, phases=True):
 
 
 @pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
-def test_loopback_partitions_rmat(parts, port):
+@pytest.mark.parametrize("scope", ["gpu", "sys"])
+def test_loopback_partitions_rmat(parts, scope, port, monkeypatch):
+    # scope=sys: the system-scope exchange a multi-GPU placement uses
+    # (PBFS_MULTI_SYS_SCOPE test hook), run on one GPU.
+    monkeypatch.setenv("PBFS_MULTI_SYS_SCOPE", "1" if scope == "sys" else "0")
     g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 16, 16, 1,
                                      drop_self_loops=True))
     mg = g.multi_device([0] * parts)
@@ -93,3 +97,22 @@ def test_rejects_unsupported_configs():
         mg.bfs(g.vertex_count, pb.KernelConfig(variant=pb.KernelVariant.Hybrid))
     with pytest.raises(pb.ConfigError):
         g.multi_device([0] * 9)
+
+
+def test_run_bfs_reaches_the_multi_engine_through_graph_options(port):
+    # pbfs_graph_options.devices: run_bfs (kernels.cpp:657-691) on a handle
+    # partitioned over a device list, the path a KernelFn takes.
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 14, 16, 3,
+                                     drop_self_loops=True))
+    stats = pb.compute_stats(g)
+    for s in pb.pick_sources(g, 3, 5):
+        want = port.bfs_serial(g.row_offsets, g.column_indices, int(s))
+        r = pb.run_bfs(g, int(s), pb.KernelConfig(variant=pb.KernelVariant.Hybrid), stats,
+                       device=[0, 0, 0])
+        assert np.array_equal(r.distances, want)
+        assert [int(x.phase) for x in r.trace.records] == port.simulate_phases(g.row_offsets, want)
+    dg = g.device([0, 0, 0])
+    assert dg.info["partitions"] == 3
+    dg.bfs_async(int(pb.pick_sources(g, 1, 5)[0]), pb.KernelConfig(variant=pb.KernelVariant.Hybrid))
+    dg.sync()
+    assert dg.component()[0] > 0

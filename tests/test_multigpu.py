@@ -172,3 +172,79 @@ def test_device_relabel_matches_model():
     for v in [0, 1, 2, 777, g.vertex_count - 1]:
         pb.parbfs._check(pb.parbfs.lib.pbfs_part_relabel(p.h, v, ctypes.byref(out)))
         assert out.value == int(gid[v])
+
+
+class _DevView:
+    """Zero-copy torch view of library-owned device memory (int32 words)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _cuda_engine_worker(rank, world, port, out):
+    # One rank of the per-level partitioned engine (pbfs_part.cu, the real
+    # CUDA kernels) per process, both on cuda:0; the per-level exchange is a
+    # gloo allgather of the next-bitmap slices staged through host memory
+    # (bench.py's PBFS_DIST_BACKEND=gloo mode). Kernels of the two ranks never
+    # wait on each other: the ranks meet only in the host collective.
+    import torch
+    import oracle
+    import paper_2503_00430_b200 as pb
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 2,
+                                     drop_self_loops=True))
+    part = pb.PartitionedGraph(g.device(0, 8), rank, world)
+    info = part.info()
+    wl, wt = info["words_local"], info["words_total"]
+    cfg = pb.KernelConfig(variant=pb.KernelVariant.Hybrid)
+    port_lib = oracle.port()
+    ok, phases_ok = True, True
+    for s in [int(x) for x in pb.pick_sources(g, 4, 6)]:
+        part.begin(s, cfg)
+        recs = []
+        while True:
+            part.step()
+            part.sync()
+            nxt = part.info()["next"]
+            view = torch.as_tensor(_DevView(nxt, wt), device="cuda")  # the full next bitmap
+            mine = view[rank * wl:(rank + 1) * wl].cpu()
+            gathered = torch.empty(wt, dtype=torch.int32)
+            dist.all_gather_into_tensor(gathered, mine)
+            view.copy_(gathered)
+            torch.cuda.synchronize()
+            done, rec = part.end_level()
+            recs.append(int(rec.phase))
+            if done:
+                break
+        local = part.local_distances()
+        allp = [None] * world
+        dist.all_gather_object(allp, local.tolist())
+        if rank == 0:
+            dist_pi = np.concatenate([np.array(a, dtype=np.uint32) for a in allp])
+            got = part.unrelabel_host(dist_pi)
+            want = port_lib.bfs_serial(g.row_offsets, g.column_indices, s)
+            ok &= bool(np.array_equal(got, want))
+            phases_ok &= recs == port_lib.simulate_phases(g.row_offsets, want)
+    if rank == 0:
+        out.put((ok, phases_ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_process_cuda_partition_engine_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cuda_engine_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok, phases_ok = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok, "2-process partitioned distances differ from the oracle"
+    assert phases_ok, "2-process partitioned phases differ from the reference rule"
