@@ -15,8 +15,10 @@
 // so a KernelFn called per source does not re-upload.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <span>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -58,6 +60,7 @@ inline pbfs_config to_c(const KernelConfig& c) {
   out.force_top_down_only = c.force_top_down_only ? 1u : 0u;
   out.validate_same_value_stores = c.validate_same_value_stores ? 1u : 0u;
   out.racy_visited_claim = c.racy_visited_claim ? 1u : 0u;
+  out.observe_frontiers = c.level_observer ? 1u : 0u;
   return out;
 }
 
@@ -201,6 +204,29 @@ inline BfsResult bfs_on(pbfs_graph* h, VertexId source, const KernelConfig& conf
   r.trace.same_value_violations = info.same_value_violations;
   r.trace.total_elapsed =
       std::chrono::nanoseconds(static_cast<std::int64_t>(info.device_ms * 1e6));
+  if (config.level_observer) {
+    // LevelObserver (kernel_config.hpp:26-36, kernels.cpp:158-161,466-481):
+    // the seed frontier, then every produced frontier as the device formed
+    // it -- top-down levels in the device's push order, bottom-up levels as
+    // ascending distinct ids.
+    std::uint64_t total = 0;
+    throw_status(pbfs_graph_observed(h, nullptr, 0, &total));
+    std::vector<VertexId> log(total);
+    throw_status(pbfs_graph_observed(h, log.data(), total, &total));
+    const VertexId seed[1] = {source};
+    config.level_observer(LevelSnapshot{0, TraversalPhase::TopDown, std::span<const VertexId>(seed, 1)});
+    std::uint64_t pos = 0;
+    for (std::uint32_t d = 1; d < got; ++d) {
+      const std::uint64_t k = levels[d].distinct_size;
+      if (pos + k > log.size()) throw CorrectnessError("observed frontiers shorter than the trace");
+      const bool bu = levels[d - 1].phase != 0;
+      if (bu) std::sort(log.begin() + static_cast<std::ptrdiff_t>(pos),
+                        log.begin() + static_cast<std::ptrdiff_t>(pos + k));
+      config.level_observer(LevelSnapshot{d, bu ? TraversalPhase::BottomUp : TraversalPhase::TopDown,
+                                          std::span<const VertexId>(log.data() + pos, k)});
+      pos += k;
+    }
+  }
   r.trace.records.reserve(got);
   for (std::uint32_t i = 0; i < got; ++i) {
     LevelRecord rec;

@@ -51,7 +51,12 @@ typedef enum pbfs_variant {
   PBFS_HYBRID_BEAMER = 4,    /* TD/BU by Beamer alpha/beta (kernels.cpp:498-511) */
   PBFS_VISITED_INLINE = 5,   /* hybrid, visited-bitmap claim, inline dist (kernels.cpp:302-320) */
   PBFS_VISITED_DEFERRED = 6,
-  PBFS_PERIODIC_FLUSH = 7
+  PBFS_PERIODIC_FLUSH = 7,
+  /* GPU addition: the reference's own Hybrid claim discipline -- top-down
+   * with PlainStore (probe dist, plain same-value store, no atomic; racing
+   * writers may all push, kernels.cpp:291-301) and bottom-up, 5 % rule
+   * (kernels.cpp:606-616). PBFS_HYBRID runs the visited-bitmap claim. */
+  PBFS_HYBRID_PLAIN = 8
 } pbfs_variant;
 
 typedef enum pbfs_phase { PBFS_TOP_DOWN = 0, PBFS_BOTTOM_UP = 1 } pbfs_phase;
@@ -82,7 +87,10 @@ typedef struct pbfs_config {
   uint32_t force_top_down_only;
   uint32_t validate_same_value_stores;
   uint32_t racy_visited_claim;
-  uint32_t reserved;
+  /* Test instrumentation (KernelConfig::level_observer, kernel_config.hpp:
+   * 26-36): record every produced frontier as it is formed on the device
+   * (pbfs_graph_observed reads them back). Off in measurements. */
+  uint32_t observe_frontiers;
 } pbfs_config;
 
 /* parbfs::LevelRecord (core/include/parbfs/trace.hpp:26-35). */
@@ -204,6 +212,13 @@ pbfs_status pbfs_graph_sync(pbfs_graph* g, void* stream);
  * levels_cap grows it). */
 pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_cap,
                              uint32_t* count);
+
+/* The frontiers the last traversal produced, recorded when it ran with
+ * cfg.observe_frontiers: the snapshots of depths 1, 2, ... concatenated
+ * (depth d's has levels[d].distinct_size entries; top-down levels in the
+ * order the device produced them, bottom-up levels as a set, any order).
+ * Copies min(total, cap) entries; *count = total. */
+pbfs_status pbfs_graph_observed(pbfs_graph* g, uint32_t* out, uint64_t cap, uint64_t* count);
 
 /* Device pointer of the distance array written by the last traversal. */
 pbfs_status pbfs_graph_device_dist(pbfs_graph* g, uint32_t** dist_dev);

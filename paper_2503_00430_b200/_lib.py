@@ -31,7 +31,7 @@ class Config(ctypes.Structure):
                 ("hybrid_threshold_fraction", c_dbl), ("alpha", c_dbl), ("beta", c_dbl),
                 ("flush_capacity", c_u64), ("force_top_down_only", c_u32),
                 ("validate_same_value_stores", c_u32), ("racy_visited_claim", c_u32),
-                ("reserved", c_u32)]
+                ("observe_frontiers", c_u32)]
 
 
 class Level(ctypes.Structure):
@@ -106,6 +106,7 @@ SIGNATURES = [
     ("pbfs_bfs_async", ctypes.c_int, [c_vp, c_u32, P(Config), c_vp]),
     ("pbfs_graph_sync", ctypes.c_int, [c_vp, c_vp]),
     ("pbfs_graph_trace", ctypes.c_int, [c_vp, P(Level), c_u32, P(c_u32)]),
+    ("pbfs_graph_observed", ctypes.c_int, [c_vp, c_vp, c_u64, P(c_u64)]),
     ("pbfs_graph_device_dist", ctypes.c_int, [c_vp, P(c_vp)]),
     ("pbfs_graph_component", ctypes.c_int, [c_vp, P(c_u64), P(c_u64)]),
     ("pbfs_host_alloc", ctypes.c_int, [ctypes.c_size_t, P(c_vp)]),

@@ -237,6 +237,8 @@ struct pbfs_graph {
   bool poisoned = false;  // a launch failed; ctl must be reset
   // pbfs_bfs_batch state, created on first use.
   uint32_t* dist2 = nullptr;
+  uint32_t* obs = nullptr;  // observer log (allocated on the first observed run)
+  uint64_t obs_cap = 0;
   cudaStream_t copy_stream = nullptr;
   int batch_slots = 0;
   cudaEvent_t kern_done[kMaxBatchSlots] = {}, copy_done[kMaxBatchSlots] = {};
@@ -328,6 +330,10 @@ pbfs_status map_variant(const pbfs_config* c, bool* hybrid_like, Launch* out) {
       *out = {kClaimBitmap, c->force_top_down_only ? kPolicyTopDown : kPolicyBeamer};
       *hybrid_like = true;
       return PBFS_OK;
+    case PBFS_HYBRID_PLAIN:
+      *out = {kClaimPlain, c->force_top_down_only ? kPolicyTopDown : kPolicyFraction};
+      *hybrid_like = true;
+      return PBFS_OK;
     case PBFS_SERIAL:
       return fail(PBFS_E_CONFIG, "the serial variant is the CPU oracle, not a GPU kernel");
     case PBFS_VISITED_DEFERRED:
@@ -342,10 +348,10 @@ pbfs_status map_variant(const pbfs_config* c, bool* hybrid_like, Launch* out) {
 
 // Latency mode (pbfs_kernels.cuh: td_phase_latency): the visited-bitmap
 // claim run top-down only on a graph without hubs. PBFS_LATENCY=0 disables it.
-bool latency_mode(const pbfs_graph* g, int claim, int policy) {
+bool latency_mode(const pbfs_graph* g, int claim, int policy, bool observe) {
   const char* e = std::getenv("PBFS_LATENCY");
   const bool off = e && e[0] == '0';
-  return !off && g->lq[0] && claim == kClaimBitmap && policy == kPolicyTopDown;
+  return !off && !observe && g->lq[0] && claim == kClaimBitmap && policy == kPolicyTopDown;
 }
 
 template <int C, typename OffT>
@@ -365,7 +371,9 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.queue[1] = g->queue[1];
   p.lq[0] = g->lq[0];
   p.lq[1] = g->lq[1];
-  p.latency = latency_mode(g, C, policy) ? 1 : 0;
+  p.latency = latency_mode(g, C, policy, cfg->observe_frontiers != 0) ? 1 : 0;
+  p.obs = cfg->observe_frontiers ? g->obs : nullptr;
+  p.obs_cap = g->obs_cap;
   p.heavy = g->heavy;
   p.ctl = g->ctl;
   p.records = g->records;
@@ -477,6 +485,11 @@ pbfs_status prologue(pbfs_graph* g, uint32_t source, const pbfs_config* cfg, Lau
   }
   PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
   if ((st = order_after_last(g, s)) != PBFS_OK) return st;
+  if (cfg->observe_frontiers && !g->obs) {
+    // Every vertex is produced once (distinct snapshots): n entries suffice.
+    g->obs_cap = g->n + 64;
+    if ((st = dalloc(g, &g->obs, g->obs_cap * 4)) != PBFS_OK) return st;
+  }
   if (g->poisoned) {
     // On the launching stream, after the previous launch: never under a
     // running traversal.
@@ -634,6 +647,12 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
     for (uint64_t v = n; v < static_cast<uint64_t>(g->words) * 32; ++v) mask[v >> 5] |= 1u << (v & 31);
   }
   g->qcap = n + g->max_degree;
+  // Test hooks: shrink the frontier queue / hub-item capacities so the
+  // device-side overflow -> PBFS_E_CAPACITY path (frontier.hpp:88-93) runs.
+  if (const char* q = std::getenv("PBFS_TEST_QCAP")) g->qcap = std::min<uint64_t>(g->qcap, std::strtoull(q, nullptr, 0));
+  if (const char* h = std::getenv("PBFS_TEST_HEAVY_CAP")) {
+    g->heavy_cap = std::min<uint64_t>(g->heavy_cap, std::strtoull(h, nullptr, 0));
+  }
   g->rec_cap = static_cast<uint32_t>(std::min<uint64_t>(n + 1, 1u << 20));
 
   int prev = 0;
@@ -1121,6 +1140,22 @@ pbfs_status pbfs_graph_trace(pbfs_graph* g, pbfs_level* levels, uint32_t levels_
   if (nlev > g->rec_cap) {
     return fail(PBFS_E_CAPACITY, "the last traversal was deeper than the device trace buffer");
   }
+  return PBFS_OK;
+}
+
+pbfs_status pbfs_graph_observed(pbfs_graph* g, uint32_t* out, uint64_t cap, uint64_t* count) {
+  if (!g || !count || (cap && !out)) return fail(PBFS_E_INPUT, "null argument");
+  if (g->multi) return fail(PBFS_E_CONFIG, "frontier observation runs on single-device handles");
+  std::lock_guard<std::mutex> lock(g->mu);
+  PBFS_CUDA(cudaSetDevice(g->device), "cudaSetDevice");
+  PBFS_CUDA(cudaEventSynchronize(g->order_ev), "traversal");
+  if (!g->obs) return fail(PBFS_E_CONFIG, "no traversal ran with observe_frontiers");
+  unsigned int total = 0;
+  PBFS_CUDA(cudaMemcpy(&total, &g->ctl->obs_count, sizeof(total), cudaMemcpyDeviceToHost),
+            "read control");
+  const uint64_t k = std::min<uint64_t>(total, cap);
+  if (k) PBFS_CUDA(cudaMemcpy(out, g->obs, k * 4, cudaMemcpyDeviceToHost), "read observed frontiers");
+  *count = total;
   return PBFS_OK;
 }
 

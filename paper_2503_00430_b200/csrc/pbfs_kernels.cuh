@@ -168,7 +168,7 @@ struct alignas(128) Ctl {
   unsigned int overflow;  // PBFS_E_CAPACITY raised on device
   unsigned int levels;
   unsigned int bu_levels;
-  unsigned int pad2;
+  unsigned int obs_count;  // observer log: entries appended by bottom-up levels' compaction
   unsigned long long reached;
   unsigned long long violations;
   unsigned long long edges;
@@ -215,6 +215,11 @@ struct Params {
   // mesh): 16 B queue entries {v, degree, row offset lo, hi}, see td_phase_latency.
   uint4* lq[2];
   int latency;
+  // Observer log (test instrumentation, kernel_config.hpp:26-36): every
+  // produced frontier appended as it was formed -- top-down the next queue
+  // (as pushed), bottom-up the produced bitmap's ids; nullptr = off.
+  uint32_t* obs;
+  unsigned long long obs_cap;
   uint32_t source;
   int policy;
   int validate;
@@ -1217,6 +1222,35 @@ __device__ __forceinline__ void front_from_dist(const uint32_t* __restrict__ dis
   }
 }
 
+// Plain-store top-down (kClaimPlain) keeps no visited bits: entering
+// bottom-up, both come from dist in one coalesced pass -- visited = reached
+// (or isolated / padding), frontier = dist == nd.
+__device__ __forceinline__ void visited_front_from_dist(const uint32_t* __restrict__ dist, uint32_t nd,
+                                                        uint32_t* visited, uint32_t* front,
+                                                        uint32_t words, unsigned long long n,
+                                                        const uint32_t* init_mask) {
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       w < words; w += nthreads) {
+    const unsigned long long base = w * 32;
+    uint32_t reached = 0, bits = 0;
+    if (base < n) {
+      const uint4* d4 = reinterpret_cast<const uint4*>(dist + base);  // dist padded to 32
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 a = __ldcs(d4 + q);
+        reached |= (uint32_t)(a.x != kUnreached) << (4 * q) | (uint32_t)(a.y != kUnreached) << (4 * q + 1) |
+                   (uint32_t)(a.z != kUnreached) << (4 * q + 2) | (uint32_t)(a.w != kUnreached) << (4 * q + 3);
+        bits |= (uint32_t)(a.x == nd) << (4 * q) | (uint32_t)(a.y == nd) << (4 * q + 1) |
+                (uint32_t)(a.z == nd) << (4 * q + 2) | (uint32_t)(a.w == nd) << (4 * q + 3);
+      }
+    }
+    const uint32_t mask = __ldg(&init_mask[w]);
+    visited[w] = reached | mask;
+    front[w] = bits & ~mask;
+  }
+}
+
 template <int C, typename OffT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
   __shared__ __align__(16) uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
@@ -1264,6 +1298,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       }
       ctl->overflow = 0;
       ctl->violations = 0;
+      ctl->obs_count = 0;
     }
   }
   const unsigned long long src_deg = degree_of(p, src);
@@ -1287,6 +1322,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
   unsigned long long cur_raw = 1, cur_distinct = 1;
   unsigned long long reached = 0, edges_total = 0;
   unsigned int bu_levels = 0;
+  unsigned long long obs_pos = 0;  // observer log fill (identical in every CTA)
   unsigned long long t_start = leader ? globaltimer() : 0;
   bar.sync();
 
@@ -1355,8 +1391,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     tl_mark(1);
     bar.sync(cnt);
     tl_mark(2);
-    if constexpr (C == kClaimPlain) {
-      // BFS-NonAtomic: the marks collapse into the distinct next frontier.
+    if (C == kClaimPlain && td) {
+      // BFS-NonAtomic / plain-store hybrid: the marks collapse into the
+      // distinct next frontier (the reference counts it with its seen_ scan,
+      // kernels.cpp:409-420).
       compact_bitmap(p.bm[1], p.queue[qcur ^ 1], p.words, &cnt->conv_count, true, nullptr,
                      p.force & kForceWideCompact);
       bar.sync(cnt);
@@ -1365,7 +1403,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
     const unsigned long long produced =
-        C == kClaimPlain ? (unsigned long long)snap.conv_count() : snap.produced();
+        C == kClaimPlain && td ? (unsigned long long)snap.conv_count() : snap.produced();
     const unsigned long long raw = td ? snap.raw() : produced;
     const unsigned long long edges = snap.edges();
     const unsigned long long pdeg = snap.degree();
@@ -1400,6 +1438,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     reached += cur_distinct;
     edges_total += edges;
     bu_levels += td ? 0 : 1;
+    if (p.obs && produced > 0 && !(td && p.latency)) {
+      // Observer snapshot of the frontier this level produced (emit_snapshot,
+      // kernels.cpp:466-481): the next queue as pushed (top-down; the claims
+      // are exclusive, or for plain stores collapsed into the distinct set),
+      // or the produced bitmap's ids (bottom-up; the host sorts them
+      // ascending). Entries land at obs_pos, which every CTA tracks
+      // identically; ctl->obs_count follows it (bottom-up appends reserve
+      // through it).
+      if (obs_pos + produced > p.obs_cap) {
+        if (leader) atomicExch(&ctl->overflow, 1u);
+      } else if (td) {
+        const uint32_t* qn = p.queue[qcur ^ 1];
+        for (unsigned long long i = tid; i < produced; i += nthreads) p.obs[obs_pos + i] = qn[i];
+        if (leader) ctl->obs_count = (unsigned int)(obs_pos + produced);
+      } else {
+        compact_bitmap(p.bm[fcur], p.obs, p.words, &ctl->obs_count, false);
+        bar.sync();  // before any conversion clears the bitmap
+      }
+      obs_pos += produced;
+    }
     if (raw == 0) break;
     unvisited_edges -= pdeg;
     const unsigned long long consumed = cur_distinct;
@@ -1412,13 +1470,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     } else if (!td && next_td) {
       // Entering top-down: a queue from the produced bitmap
       // (count_bitmap_slice / write_dense_slice, kernels.cpp:225-241).
-      compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, false, nullptr,
-                     p.force & kForceWideCompact);
+      // Plain-store top-down marks into bm[1] and needs it zero: this pass
+      // clears the consumed bitmap and zeroes the other one.
+      compact_bitmap(p.bm[fcur], p.queue[qcur], p.words, &cnt->conv_count, C == kClaimPlain,
+                     C == kClaimPlain ? p.bm[fcur ^ 1] : nullptr, p.force & kForceWideCompact);
       bar.sync(cnt);
       qlen = snap.conv_count();
     } else if (C == kClaimBitmap && td && !next_td) {
       // Entering bottom-up: the frontier bitmap from this level's distances.
       front_from_dist(p.dist, depth + 1, p.bm[fcur], p.words, p.n, p.visited, p.init_mask);
+      bar.sync();
+    } else if (C == kClaimPlain && td && !next_td) {
+      // Entering bottom-up after plain-store top-down levels (no visited
+      // bits kept): visited and the frontier bitmap from dist.
+      visited_front_from_dist(p.dist, depth + 1, p.visited, p.bm[fcur], p.words, p.n, p.init_mask);
       bar.sync();
     }
     // bottom-up -> bottom-up: nothing to convert.

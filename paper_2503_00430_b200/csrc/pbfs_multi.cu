@@ -637,28 +637,41 @@ pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices, uint3
     i = j;
   }
   // Descriptors (identical bytes on every device: unified addressing).
-  // Per device: one block of every local partition's visited | bm[0] | bm[1].
+  // Per device: one block holding every local partition's visited slice,
+  // then their full bitmaps. The launch's persisting-L2 window covers the
+  // whole block when the device holds one partition (its probe working set,
+  // as in the single-GPU engine); with several partitions on one device
+  // (loopback) only the visited slices -- the replicated full bitmaps would
+  // crowd the set-aside (PBFS_MULTI_WINDOW=all|visited|none overrides).
   std::vector<uint32_t*> vis(num_partitions), bm0(num_partitions), bm1(num_partitions);
+  const char* wenv = std::getenv("PBFS_MULTI_WINDOW");
   for (auto& grp : m->groups) {
     MCUDA(cudaSetDevice(grp.device), "cudaSetDevice");
-    size_t words = 0;
+    size_t vwords = 0, words = 0;
     for (uint32_t i = grp.first; i < grp.first + grp.count; ++i) {
+      vwords += m->parts[i]->lwords;
       words += m->parts[i]->lwords + 2 * m->parts[i]->words_total;
     }
-    grp.bitmap_bytes = words * 4;
-    MCUDA(cudaMalloc(&grp.bitmaps, grp.bitmap_bytes), "bitmap block");
+    MCUDA(cudaMalloc(&grp.bitmaps, words * 4), "bitmap block");
     uint32_t* at = grp.bitmaps;
     for (uint32_t i = grp.first; i < grp.first + grp.count; ++i) {
       vis[i] = at;
       at += m->parts[i]->lwords;
+    }
+    for (uint32_t i = grp.first; i < grp.first + grp.count; ++i) {
       bm0[i] = at;
       at += m->parts[i]->words_total;
       bm1[i] = at;
       at += m->parts[i]->words_total;
     }
+    bool all = grp.count == 1;
+    if (wenv && std::strcmp(wenv, "all") == 0) all = true;
+    if (wenv && std::strcmp(wenv, "visited") == 0) all = false;
+    grp.bitmap_bytes = (all ? words : vwords) * 4;
     cudaDeviceProp prop;
     MCUDA(cudaGetDeviceProperties(&prop, grp.device), "props");
-    if (prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0) {
+    const bool none = wenv && std::strcmp(wenv, "none") == 0;
+    if (!none && prop.persistingL2CacheMaxSize > 0 && prop.accessPolicyMaxWindowSize > 0) {
       grp.bitmap_bytes = std::min<size_t>(grp.bitmap_bytes, prop.accessPolicyMaxWindowSize);
       const size_t want = std::min<size_t>(grp.bitmap_bytes, prop.persistingL2CacheMaxSize);
       size_t cur = 0;
@@ -700,7 +713,10 @@ pbfs_status pbfs_multi_create(const pbfs_csr* csr, const int32_t* devices, uint3
     d.td.visited = d.bu.visited = vis[i];
     d.td.heavy = heavy[i];
     d.td.heavy_cap = heavy_cap[i];
-    d.td.small_chunks = 1;
+    {
+      const char* sc = std::getenv("PBFS_MULTI_SMALL_CHUNKS");  // A/B knob
+      d.td.small_chunks = sc && sc[0] == '0' ? 0 : 1;
+    }
     if (g->m_loc >= kBigArcs) {
       d.td.heavy_deg = kHeavyDegBig;
       d.td.chunk_log2 = __builtin_ctz(kChunkBig);

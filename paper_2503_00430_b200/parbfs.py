@@ -88,6 +88,9 @@ class KernelVariant(enum.IntEnum):
     VisitedBitmapInline = 5
     VisitedBitmapDeferred = 6
     TopDownPeriodicFlush = 7
+    # GPU addition (pbfs.h PBFS_HYBRID_PLAIN): the reference Hybrid's own
+    # PlainStore top-down claim (no atomic) with the 5 % switch.
+    HybridPlainStore = 8
 
 
 class TraversalPhase(enum.IntEnum):
@@ -113,6 +116,7 @@ _VARIANT_TOKENS = {
     KernelVariant.VisitedBitmapInline: "visited-inline",
     KernelVariant.VisitedBitmapDeferred: "visited-deferred",
     KernelVariant.TopDownPeriodicFlush: "periodic-flush",
+    KernelVariant.HybridPlainStore: "hybrid-plain",
 }
 
 
@@ -166,6 +170,7 @@ class KernelConfig:
         c.force_top_down_only = int(bool(self.force_top_down_only))
         c.validate_same_value_stores = int(bool(self.validate_same_value_stores))
         c.racy_visited_claim = int(bool(self.racy_visited_claim))
+        c.observe_frontiers = int(self.level_observer is not None)
         return c
 
 
@@ -504,6 +509,8 @@ class BfsResult:
     """kernels.hpp:15-20: uint32 distances (kUnreached = 0xFFFFFFFF = int32 -1)."""
     distances: np.ndarray
     trace: TraversalTrace
+    # Device-recorded frontiers (cfg.level_observer set), for _emit_snapshots.
+    _observed: Optional[np.ndarray] = None
 
 
 # ---- device graph + traversal -------------------------------------------------------
@@ -637,6 +644,13 @@ class DeviceGraph:
                                 dist.ctypes.data if dist is not None else None, levels, cap,
                                 ctypes.byref(info)))
         t1 = time.perf_counter_ns()
+        observed = None
+        if config.level_observer is not None:
+            total = ctypes.c_uint64()
+            _check(lib.pbfs_graph_observed(self.h, None, 0, ctypes.byref(total)))
+            observed = np.empty(total.value, dtype=np.uint32)
+            _check(lib.pbfs_graph_observed(self.h, observed.ctypes.data, observed.size,
+                                           ctypes.byref(total)))
         trace = TraversalTrace(variant=KernelVariant(config.variant),
                                worker_count=config.worker_count, source=int(source),
                                same_value_violations=int(info.same_value_violations),
@@ -647,7 +661,7 @@ class DeviceGraph:
                 trace.records.append(LevelRecord(r.depth, TraversalPhase(r.phase), r.frontier_size,
                                                  r.distinct_size, r.duplicate_count,
                                                  r.edges_examined, r.flush_events, r.elapsed_ns))
-        return BfsResult(dist, trace)
+        return BfsResult(dist, trace, observed)
 
     def bfs_batch(self, sources, config: KernelConfig, outs,
                   widths: Optional[list] = None) -> List[float]:
@@ -723,20 +737,27 @@ class LevelSnapshot:
 
 def _emit_snapshots(result: BfsResult, observer: Callable) -> None:
     """LevelObserver parity (kernels.cpp:158-161,466-481): one snapshot for the
-    seed frontier, then one per produced level, in depth order. The device
-    frontiers carry no duplicates (claims are exact), so each snapshot is the
-    ascending set of vertices first reached at that depth -- what the
-    reference's observers see after their sort + unique."""
-    d = result.distances
-    reached = d != UNREACHED
-    order = np.argsort(d[reached], kind="stable")
-    ids = np.nonzero(reached)[0][order].astype(np.uint32)
-    levels = d[reached][order]
-    bounds = np.searchsorted(levels, np.arange(int(levels.max()) + 2 if levels.size else 1))
+    seed frontier, then one per produced level, in depth order, carrying the
+    frontier the DEVICE produced (recorded with cfg.observe_frontiers,
+    pbfs_graph_observed): top-down levels as the device pushed them (its
+    order), bottom-up levels as ascending ids (the reference scans its byte
+    bitmap in id order)."""
     recs = result.trace.records
-    for depth in range(len(bounds) - 1):
-        phase = TraversalPhase.TopDown if depth == 0 else recs[depth - 1].phase
-        observer(LevelSnapshot(depth, phase, ids[bounds[depth]:bounds[depth + 1]]))
+    log = result._observed
+    observer(LevelSnapshot(0, TraversalPhase.TopDown,
+                           np.array([result.trace.source], dtype=np.uint32)))
+    pos = 0
+    for depth in range(1, len(recs)):
+        k = recs[depth].distinct_size
+        entries = log[pos:pos + k]
+        pos += k
+        phase = recs[depth - 1].phase
+        if phase == TraversalPhase.BottomUp:
+            entries = np.sort(entries)
+        observer(LevelSnapshot(depth, phase, entries))
+    if pos != log.size:
+        raise CorrectnessError(f"observed {log.size} frontier entries, the trace accounts "
+                               f"for {pos}")
 
 
 def _gpu_run(graph: CsrGraph, source: int, config: KernelConfig, variant: KernelVariant,
@@ -765,6 +786,13 @@ def bfs_nonatomic(graph: CsrGraph, source: int, config: KernelConfig) -> BfsResu
 def bfs_hybrid(graph: CsrGraph, source: int, config: KernelConfig) -> BfsResult:
     """kernels.cpp:606-616: direction switch by the frontier-size fraction."""
     return _gpu_run(graph, source, config, KernelVariant.Hybrid)
+
+
+def bfs_hybrid_plain(graph: CsrGraph, source: int, config: KernelConfig) -> BfsResult:
+    """kernels.cpp:606-616 with the reference Hybrid's own claim discipline:
+    PlainStore top-down (no atomic, kernels.cpp:291-301) + bottom-up, 5 %
+    switch (GPU variant PBFS_HYBRID_PLAIN)."""
+    return _gpu_run(graph, source, config, KernelVariant.HybridPlainStore)
 
 
 def bfs_hybrid_beamer(graph: CsrGraph, source: int, config: KernelConfig) -> BfsResult:

@@ -16,9 +16,11 @@ from graphs import (from_edges, hand_suite, make_circulant, make_complete_bipart
 pytestmark = pytest.mark.gpu
 UNREACHED = 0xFFFFFFFF
 V = pb.KernelVariant
-GPU_VARIANTS = [V.Conventional, V.NonAtomic, V.Hybrid, V.HybridBeamer, V.VisitedBitmapInline]
+GPU_VARIANTS = [V.Conventional, V.NonAtomic, V.Hybrid, V.HybridBeamer, V.VisitedBitmapInline,
+                V.HybridPlainStore]
 DIRECT = {V.Conventional: pb.bfs_conventional, V.NonAtomic: pb.bfs_nonatomic,
           V.Hybrid: pb.bfs_hybrid, V.HybridBeamer: pb.bfs_hybrid_beamer,
+          V.HybridPlainStore: pb.bfs_hybrid_plain,
           V.VisitedBitmapInline: lambda g, s, c: pb.bfs_visited_bitmap(g, s, c, False)}
 
 
