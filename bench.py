@@ -355,7 +355,24 @@ class _DeviceArray:
                                          "strides": None}
 
 
+def build_hash() -> str:
+    """sha256 over the library sources: a traffic capture belongs to exactly
+    the build it was taken from."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2503_00430_b200", "csrc")
+    files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cuh", ".h", ".cpp")) or
+                   f == "Makefile")
+    for f in files:
+        h.update(f.encode())
+        h.update(open(os.path.join(csrc, f), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "pbfs.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def _peak_and_traffic(workload):
+    """Measured HBM peak, and the ncu traffic capture of this workload if it
+    was taken from the current build (tools/capture_traffic.py)."""
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -365,7 +382,12 @@ def _peak_and_traffic(workload):
     tpath = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            t = json.load(open(tpath))
+            if t.get("build_hash") == build_hash() and t.get("variant", "hybrid") == VARIANT:
+                traffic = t
+            else:
+                log(f"[bench] {tpath} was captured for build {t.get('build_hash')}, "
+                    f"not {build_hash()}: traffic not reported")
         except (OSError, ValueError):
             traffic = None
     return float(peaks.get("hbm_gbs", 6650.0)), traffic
@@ -632,7 +654,17 @@ def run_single(args):
     gteps = [er / (t * 1e-3) / 1e9 for _, er, _, t in rows]
     value = harmonic(gteps)
     achieved = sum(b for _, _, b, _ in rows) / sum(t * 1e-3 for _, _, _, t in rows) / 1e9
-    peak, traffic = _peak_and_traffic(args.workload)
+    peak, tcap = _peak_and_traffic(args.workload)
+    traffic = dram_frac = None
+    if tcap:
+        # bytes actually moved (ncu, same build) over the live device time of
+        # the same sources: "bytes actually moved per BFS over peak bandwidth"
+        per = [x for x in tcap["per_source"] if x["source"] in t_src]
+        if per:
+            moved = sum(x["dram_bytes_read"] + x["dram_bytes_write"] for x in per)
+            secs = sum(t_src[x["source"]] * 1e-3 for x in per)
+            traffic = moved / len(per)
+            dram_frac = moved / secs / 1e9 / peak
 
     # e2e: the public API with host buffers (pinned), the D2H of every
     # distance array inside the timed region. Headline: pbfs_bfs_batch over
@@ -688,8 +720,14 @@ def run_single(args):
                                             t for *_, t in rows), 4)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "dram_frac": round(dram_frac, 4) if dram_frac is not None else None,
+                     "traffic_capture": ({"file": f"profiles/traffic_{args.workload}.json",
+                                          "build_hash": tcap["build_hash"],
+                                          "sources": tcap["sources"]} if tcap else None),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
                      "kernel": "bfs_persistent (one cooperative launch per BFS)",
-                     "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source"},
+                     "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source; "
+                                    "dram_frac = ncu dram bytes / (t x peak)"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 4 * NUM_SOURCES,
