@@ -411,6 +411,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plugin-sources", type=int, default=16,
+                    help="sources for the C++ KernelFn per-call e2e (0 = skip)")
     ap.add_argument("--variant", default="hybrid",
                     help="GPU kernel variant (reference names: hybrid, conventional, nonatomic, "
                          "hybrid-beamer, visited-inline); the reference arm stays parbfs::bfs_hybrid")
@@ -699,6 +701,24 @@ def run_single(args):
         sync_rows.append(e_r[s] / (t1 - t0) / 1e9)
     e2e_sync = harmonic(sync_rows)
 
+    # The reference's plugin slot: KernelFn = gpu::kernel_fn() from the C++
+    # drop-in (include/parbfs_gpu.hpp), one call per source, as time_run /
+    # bfsbench would call it (tests/cpp/adapter_check.cpp percall; the graph
+    # goes through the reference's own CSR1 loader).
+    plugin = None
+    adapter = os.path.join(ROOT, "oracle", "_ref", "adapter_check")
+    if args.plugin_sources and os.path.exists(adapter):
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "graph.csr")
+            pb.save_binary_csr(graph, path)
+            r = subprocess.run([adapter, "percall", path, str(args.plugin_sources)],
+                               capture_output=True, text=True, timeout=1200)
+            lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+            if r.returncode == 0 and lines:
+                plugin = json.loads(lines[0])
+            else:
+                log(f"[bench] plugin per-call run failed: {r.stdout[-500:]} {r.stderr[-500:]}")
+
     cpu = None
     if not args.no_cpu_baseline:
         def gpu_dist(s):
@@ -740,7 +760,12 @@ def run_single(args):
                 "transfer_bytes_per_vertex": sorted(set(widths)),
                 "batch_ms_per_source": round(t_batch * 1e3, 3),
                 "parity_last_source": e2e_parity,
-                "sync_per_call_value": round(e2e_sync, 3)},
+                "sync_per_call_value": round(e2e_sync, 3),
+                "plugin_per_call_value": plugin["plugin_per_call_gteps"] if plugin else None,
+                "plugin_per_call": ({**plugin, "how": "parbfs::KernelFn = gpu::kernel_fn() "
+                                     "(include/parbfs_gpu.hpp) per source from C++, steady clock "
+                                     "around each call incl. the BfsResult's host vector"}
+                                    if plugin else None)},
         "gpu_launches": launches,
         "clocks": clk,
     }

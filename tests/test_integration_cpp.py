@@ -57,3 +57,21 @@ def test_adapter_compiles_against_reference_and_has_no_cpu_fallback(tmp_path):
         assert r.returncode == 0 and r.stdout.startswith("GPU"), r.stdout + r.stderr
     else:
         assert r.returncode == 3, r.stdout + r.stderr
+
+
+ADAPTER = os.path.join(ROOT, "oracle", "_ref", "adapter_check")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["criterion1", "timerun"])
+def test_reference_drives_the_b200_through_the_cpp_adapter(mode):
+    # tests/cpp/adapter_check.cpp, prebuilt here against the unmodified
+    # reference headers (make -C oracle adapter) and shipped with the repo:
+    # acceptance criterion 1 through gpu::run_bfs (200 graphs, each rebuilt in
+    # the same stack slot), the reference's own oracle-checked time_run over
+    # gpu::kernel_fn(), equal-sized graphs at one address, and the
+    # LevelObserver.
+    assert os.path.exists(ADAPTER), "oracle/_ref/adapter_check must travel with the repo"
+    r = subprocess.run([ADAPTER, mode], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.startswith(("OK", "time_run")), r.stdout + r.stderr
+    assert "OK" in r.stdout
