@@ -238,6 +238,10 @@ struct pbfs_graph {
   // pbfs_bfs_batch state, created on first use.
   uint32_t* dist2 = nullptr;
   uint32_t* obs = nullptr;  // observer log (allocated on the first observed run)
+  // Single calls into pageable host memory (the C++ KernelFn's std::vector):
+  // packed device copy + pinned staging + the widening pool.
+  void* pack1 = nullptr;
+  void* stage1 = nullptr;
   uint64_t obs_cap = 0;
   cudaStream_t copy_stream = nullptr;
   int batch_slots = 0;
@@ -292,6 +296,7 @@ void release(pbfs_graph* g) {
   g->widener.reset();
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   for (void* h : g->stage) if (h) cudaFreeHost(h);
+  if (g->stage1) cudaFreeHost(g->stage1);
   for (cudaEvent_t e : g->run_ev) cudaEventDestroy(e);
   for (int i = 0; i < kMaxBatchSlots; ++i) {
     if (g->kern_done[i]) cudaEventDestroy(g->kern_done[i]);
@@ -416,6 +421,10 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   }
   lc.attrs = attr;
   lc.numAttrs = nattr;
+  if (p.obs) return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT, false, true>, p);
+  if constexpr (C == kClaimBitmap) {
+    if (p.latency) return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT, true, false>, p);
+  }
   return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT>, p);
 }
 
@@ -825,8 +834,27 @@ pbfs_status pbfs_bfs_locked(pbfs_graph* g, uint32_t source, const pbfs_config* c
   pbfs_status st = prologue(g, source, cfg, &l, g->stream);
   if (st != PBFS_OK) return st;
   cudaError_t e;
+  // A large PAGEABLE destination (e.g. a std::vector behind the reference's
+  // KernelFn) would take the driver's staged pageable copy at 4 B/vertex:
+  // instead the kernel also writes 1-2 B/vertex level codes, those land in
+  // pinned staging, and the widening pool expands them into the caller's
+  // array on every host core (faulting its pages in parallel too).
+  bool packed = false;
+  if (dist_host && (g->n >= kPackMinVertices || (g->force & kForcePack))) {
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, dist_host) == cudaSuccess &&
+                        pa.type != cudaMemoryTypeUnregistered;
+    cudaGetLastError();
+    if (!pinned) {
+      const uint64_t pbytes = ((g->n + 15) / 16) * 32;
+      if (!g->pack1 && (st = dalloc(g, &g->pack1, pbytes)) != PBFS_OK) return st;
+      if (!g->stage1) PBFS_CUDA(cudaHostAlloc(&g->stage1, pbytes, cudaHostAllocDefault), "pinned staging");
+      if (!g->widener) g->widener.reset(new Widener(widen_threads()));
+      packed = true;
+    }
+  }
   PBFS_CUDA(cudaEventRecord(g->ev0, g->stream), "event record");
-  if ((e = launch(g, source, cfg, l, g->stream)) != cudaSuccess) {
+  if ((e = launch(g, source, cfg, l, g->stream, nullptr, packed ? g->pack1 : nullptr)) != cudaSuccess) {
     g->poisoned = true;
     return cuda_fail(e, "traversal launch");
   }
@@ -843,7 +871,17 @@ pbfs_status pbfs_bfs_locked(pbfs_graph* g, uint32_t source, const pbfs_config* c
     return fail(PBFS_E_CAPACITY, "dense frontier overflow");
   }
   if (dist_host) {
-    PBFS_CUDA(cudaMemcpy(dist_host, g->dist, g->n * 4, cudaMemcpyDeviceToHost), "read distances");
+    const uint32_t width = packed ? pack_width(ctl.levels) : 4u;
+    if (width < 4) {
+      PBFS_CUDA(cudaMemcpy(g->stage1, g->pack1, g->n * width, cudaMemcpyDeviceToHost), "read distances");
+      Widener& wd = *g->widener;
+      wd.reset();
+      Widener::Job job{g->stage1, dist_host, g->n, width, 0, &wd};
+      wd.submit(job);
+      wd.wait(0);
+    } else {
+      PBFS_CUDA(cudaMemcpy(dist_host, g->dist, g->n * 4, cudaMemcpyDeviceToHost), "read distances");
+    }
   }
   const uint32_t nrec = std::min<uint32_t>(ctl.levels, g->rec_cap);
   if (levels && levels_cap) {

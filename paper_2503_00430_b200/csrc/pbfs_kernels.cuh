@@ -1251,7 +1251,10 @@ __device__ __forceinline__ void visited_front_from_dist(const uint32_t* __restri
   }
 }
 
-template <int C, typename OffT>
+// kLat: latency mode (hub-free graphs run top-down only); kObs: observer
+// snapshots (test instrumentation). Separate instantiations, so neither
+// costs the general kernel registers.
+template <int C, typename OffT, bool kLat = false, bool kObs = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
   __shared__ __align__(16) uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
   __shared__ uint32_t s_found[kWarps][kGroupWords];
@@ -1287,7 +1290,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     }
     if (leader) {
       p.queue[0][0] = src;
-      if (p.latency) {
+      if (kLat) {
         const unsigned long long b = (unsigned long long)p.rowptr[src];
         p.lq[0][0] = make_uint4(src, (uint32_t)(p.rowptr[src + 1] - p.rowptr[src]), (uint32_t)b,
                                 (uint32_t)(b >> 32));
@@ -1355,7 +1358,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
 #else
     auto tl_mark = [](int) {};
 #endif
-    if (td && p.latency) {
+    if (kLat && td) {
       WarpPush4 wp4{reinterpret_cast<uint4*>(s_list[warp]), 0};
       td_phase_latency(p, depth, p.lq[qcur], qlen, p.lq[qcur ^ 1], wp4, cnt, t);
       wp4.flush(p.lq[qcur ^ 1], &cnt->raw, p.qcap, &ctl->overflow);
@@ -1438,7 +1441,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     reached += cur_distinct;
     edges_total += edges;
     bu_levels += td ? 0 : 1;
-    if (p.obs && produced > 0 && !(td && p.latency)) {
+    if (kObs && produced > 0) {
       // Observer snapshot of the frontier this level produced (emit_snapshot,
       // kernels.cpp:466-481): the next queue as pushed (top-down; the claims
       // are exclusive, or for plain stores collapsed into the distinct set),

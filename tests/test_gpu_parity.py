@@ -445,3 +445,24 @@ def test_trace_deeper_than_the_default_record_buffer(port):
     assert np.array_equal(r.distances, np.arange(n, dtype=np.uint32))
     assert len(r.trace.records) == n
     assert r.trace.records[-1].depth == n - 1 and r.trace.records[-1].distinct_size == 1
+
+
+def test_single_call_into_pageable_memory_packed(port, monkeypatch):
+    # pbfs_bfs into a PAGEABLE destination (numpy, or the C++ adapter's
+    # std::vector) takes the packed 1-2 B/vertex transfer + host widening;
+    # kForcePack (8) runs it on small graphs: 1 B codes, 2 B codes (a path of
+    # 300 levels), and the plain 4 B copy past 65534 levels.
+    monkeypatch.setenv("PBFS_FORCE_MODES", "8")
+    g = pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 9,
+                                     drop_self_loops=True))
+    dg = g.device(0, 8)
+    for s in pb.pick_sources(g, 4, 2):
+        out = np.empty(g.vertex_count, dtype=np.uint32)  # pageable
+        dg.bfs(int(s), pb.KernelConfig(variant=V.Hybrid), out=out)
+        assert np.array_equal(out, port.bfs_serial(g.row_offsets, g.column_indices, int(s)))
+    for n in (300, 70000):
+        p = make_path(n)
+        out = np.empty(n, dtype=np.uint32)
+        p.device(0, 8).bfs(0, pb.KernelConfig(variant=V.Hybrid, force_top_down_only=True),
+                           out=out, want_trace=False)
+        assert np.array_equal(out, np.arange(n, dtype=np.uint32))
