@@ -78,6 +78,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_CHUNK
 #define PBFS_CHUNK 512
 #endif
+#ifndef PBFS_LAT_SPREAD
+#define PBFS_LAT_SPREAD 1  // latency mode: adaptive slice width, slices dealt over CTAs (A/B knob)
+#endif
 constexpr int kMinBlocks = PBFS_MIN_BLOCKS;  // resident CTAs per SM the register budget targets
 // Hub split for graphs below kBigArcs directed arcs; larger graphs take
 // kHeavyDegBig / kChunkBig (their levels are long enough that fewer, larger
@@ -804,12 +807,19 @@ __device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const ui
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
   const unsigned warps_total = gridDim.x * kWarps;
-  unsigned long long base = (unsigned long long)(blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32;
+  // Slices narrower than 32 entries on a frontier smaller than one full
+  // slice per warp, dealt round-robin over the CTAs (warp-major), so a ~4 K
+  // level occupies every SM instead of the first few CTAs' warps.
+  unsigned W = 32;
+  while (PBFS_LAT_SPREAD && W > 1 && (unsigned long long)warps_total * (W / 2) >= qlen) W /= 2;
+  const unsigned gwi = PBFS_LAT_SPREAD ? (threadIdx.x >> 5) * gridDim.x + blockIdx.x
+                                       : blockIdx.x * kWarps + (threadIdx.x >> 5);
+  unsigned long long base = (unsigned long long)gwi * W;
   while (base < qlen) {
     const unsigned long long i = base + lane;
     uint32_t deg = 0;
     unsigned long long beg = 0;
-    if (i < qlen) {
+    if (lane < W && i < qlen) {
       const uint4 q = qin[i];
       deg = q.y;
       beg = (unsigned long long)q.z | ((unsigned long long)q.w << 32);
@@ -847,7 +857,7 @@ __device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const ui
         claim_latency<K>(p, nd, v, okm, qout, wp, cnt, t);
       }
     }
-    if (qlen <= (unsigned long long)warps_total * 32) break;
+    if (qlen <= (unsigned long long)warps_total * W) break;
     unsigned int nb = 0;
     if (lane == 0) nb = atomicAdd(&cnt->td_cursor, 32u);
     base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
