@@ -252,6 +252,7 @@ struct pbfs_graph {
   Ctl* ctl_host = nullptr;  // pinned, ctl_host_cap entries
   uint32_t ctl_host_cap = 0;
   std::vector<cudaEvent_t> run_ev;  // per-source start/end events (2 per source)
+  uint32_t red_minq = 0;  // reduction-claim frontier length (bfs_persistent), 0 = off
 };
 
 namespace {
@@ -400,6 +401,7 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.threshold = cfg->hybrid_threshold_fraction;
   p.alpha = cfg->alpha;
   p.beta = cfg->beta;
+  p.red_minq = g->red_minq;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(p.latency ? g->lat_grid : g->grid);
   lc.blockDim = dim3(kThreads);
@@ -792,6 +794,8 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
       g->persist_bytes = want;
     }
   }
+  g->red_minq = kRedMinQ;
+  if (const char* q = std::getenv("PBFS_RED_MINQ")) g->red_minq = static_cast<uint32_t>(std::strtoul(q, nullptr, 0));
   cudaSetDevice(prev);
   *out = g;
   return PBFS_OK;

@@ -99,6 +99,12 @@ constexpr unsigned long long kBigArcs = 1ull << 30;
 #define PBFS_SMALL_CHUNK_LOG2 8
 #endif
 constexpr unsigned long long kSmallFrontier = PBFS_SMALL_Q;
+// Reduction claim (bfs_persistent): top-down levels from this many frontier
+// vertices claim with no-return reds (per-graph override PBFS_RED_MINQ, 0 = off).
+#ifndef PBFS_RED_MINQ
+#define PBFS_RED_MINQ 65536
+#endif
+constexpr uint32_t kRedMinQ = PBFS_RED_MINQ;
 // Test hooks: run the size-gated paths on small graphs (parity coverage).
 constexpr uint32_t kForceSparseBu = 1;     // sparse bottom-up tasks at every level
 constexpr uint32_t kForceWideCompact = 2;  // 8-words-per-lane compaction
@@ -229,6 +235,7 @@ struct Params {
   double threshold;
   double alpha;
   double beta;
+  uint32_t red_minq = 0;  // reduction claim from this frontier length (0 = off; bfs_persistent)
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -464,7 +471,7 @@ template <int C, int K, typename OffT, class WP>
 __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
                                             const uint32_t (&v)[K], uint32_t okm,
                                             uint32_t* qout, WP& wp, LevelCnt* cnt,
-                                            WarpTally& t, uint32_t* obm) {
+                                            WarpTally& t, uint32_t* obm, uint32_t* rbm = nullptr) {
   // Unconditional probes (dead slots hold a valid vertex id): predicated
   // loads end up in separate blocks that ptxas interleaves with their uses,
   // serialising the round trips this batching exists to overlap.
@@ -479,6 +486,23 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
     } else {
       w[k] = probe_word<C>(p, v[k]);
     }
+  }
+  if (C == kClaimBitmap && rbm != nullptr) {
+    // Reduction claim (big top-down levels, see bfs_persistent): every slot
+    // that saw a clear visited bit stores nd (racing writers store the same
+    // value) and sets the bit in `visited` and in the next-frontier bitmap
+    // `rbm` with no-return reds -- nothing waits on a claim round trip. The
+    // distinct next frontier is the bitmap, counted and compacted after the
+    // level; a stale clear bit only costs a redundant red.
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t bit = 1u << (v[k] & 31);
+      const bool go = ((okm >> k) & 1u) && !(w[k] & bit);
+      if (go) p.dist[v[k]] = nd;
+      red_or_if(go, &p.visited[v[k] >> 5], bit);
+      red_or_if(go, &rbm[v[k] >> 5], bit);
+    }
+    return;
   }
   if constexpr (C == kClaimPlain) {
     // kernels.cpp:291-301: compare, plain store; racing writers all store the
@@ -558,7 +582,8 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
 template <int C, typename OffT, class WP>
 __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t nd, OffT beg,
                                                uint32_t deg, uint32_t* qout, WP& wp,
-                                               LevelCnt* cnt, WarpTally& t, uint32_t* obm) {
+                                               LevelCnt* cnt, WarpTally& t, uint32_t* obm,
+                                               uint32_t* rbm = nullptr) {
   constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -594,7 +619,7 @@ __device__ __forceinline__ void td_light_batch(const Params<OffT>& p, uint32_t n
       const unsigned long long ei = ok ? (unsigned long long)ob + (e - oex) : (unsigned long long)b0;
       v[k] = ld_stream(&p.col[ei]);
     }
-    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
+    claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm, rbm);
   }
 }
 
@@ -604,7 +629,7 @@ template <int C, typename OffT, class QV = const uint32_t*, class WP = WarpPush>
 __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, QV qin,
                                unsigned long long qlen, uint32_t* qout, WP& wp,
                                LevelCnt* cnt, WarpTally& t, uint32_t* obm, uint32_t* stale,
-                               VGrid vg = hw_grid()) {
+                               VGrid vg = hw_grid(), uint32_t* rbm = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
   const uint32_t nd = depth + 1;
@@ -659,7 +684,7 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, QV qin,
       }
     }
     if (hub) deg = 0;
-    td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t, obm);
+    td_light_batch<C>(p, nd, beg, (uint32_t)deg, qout, wp, cnt, t, obm, rbm);
     // The static first slices cover small frontiers entirely: no cursor
     // round trip at all (the common case on deep, narrow graphs).
     if (qlen <= (unsigned long long)warps_total * W) break;
@@ -678,7 +703,7 @@ __device__ void td_phase_light(const Params<OffT>& p, uint32_t depth, QV qin,
 template <int C, typename OffT, class WP = WarpPush>
 __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned int items,
                                uint32_t* qout, WP& wp, LevelCnt* cnt, WarpTally& t,
-                               uint32_t* obm, VGrid vg = hw_grid()) {
+                               uint32_t* obm, VGrid vg = hw_grid(), uint32_t* rbm = nullptr) {
   constexpr int K = PBFS_SLOTS;
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = lane_id();
@@ -699,7 +724,7 @@ __device__ void td_phase_heavy(const Params<OffT>& p, uint32_t depth, unsigned i
         okm |= (uint32_t)ok << k;
         v[k] = ld_stream(&base[ok ? e : 0u]);
       }
-      claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm);
+      claim_batch<C, K>(p, nd, v, okm, qout, wp, cnt, t, obm, rbm);
     }
     // Items are equal-sized (2^chunk_log2 edges but a hub's last one): a static
     // round-robin balances them without a contended cursor.
@@ -1351,6 +1376,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       ctl->cnt[(depth + 2) & 3] = z;
     }
     WarpTally t;
+    // Reduction claim (claim_batch): top-down levels of at least red_minq
+    // frontier vertices set the next frontier with no-return reds instead of
+    // returning claim atomics; the bitmap is counted and compacted after the
+    // level (the next queue for top-down, the bitmap itself for bottom-up).
+    uint32_t* red = nullptr;
+    if constexpr (C == kClaimBitmap && !kLat && !kObs) {
+      if (td && p.red_minq && qlen >= p.red_minq && p.policy != kPolicyBeamer) red = p.bm[fcur ^ 1];
+    }
 #if PBFS_TIMELINE
     // Diagnostic build: CTA 0 thread 0's view of the level (it holds the
     // first frontier slices), packed into the record's flush_events as four
@@ -1377,7 +1410,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
       uint32_t* qout = p.queue[qcur ^ 1];
       // No next-bitmap marks during the level (see front_from_dist).
       uint32_t* mark = nullptr;
-      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, nullptr);
+      if (red) {
+        // The next frontier accumulates in the bitmap that becomes bm[fcur]
+        // after this level's flip.
+        for (unsigned long long w = tid; w < p.words; w += nthreads) red[w] = 0;
+        bar.sync();
+      }
+      td_phase_light<C>(p, depth, p.queue[qcur], qlen, qout, wp, cnt, t, mark, nullptr, hw_grid(),
+                        red);
       tl_mark(0);
       if (p.max_degree > p.heavy_deg) {
         bar.sync(cnt);
@@ -1385,7 +1425,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
         const unsigned int items = (unsigned long long)snap.heavy_count() < p.heavy_cap
                                        ? snap.heavy_count()
                                        : (unsigned int)p.heavy_cap;
-        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, mark);
+        if (items) td_phase_heavy<C>(p, depth, items, qout, wp, cnt, t, mark, hw_grid(), red);
       }
       wp.flush(qout, &cnt->raw, p.qcap, &ctl->overflow);
     } else {
@@ -1412,12 +1452,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
                      p.force & kForceWideCompact);
       bar.sync(cnt);
     }
+    if (red) {
+      // The distinct next frontier: count it and write it as the next queue.
+      compact_bitmap(red, p.queue[qcur ^ 1], p.words, &cnt->conv_count, false, nullptr,
+                     p.force & kForceWideCompact);
+      bar.sync(cnt);
+    }
     if (C == kClaimBitmap || !td) fcur ^= 1;  // this level's bitmap is the latest
 
     // ---- single section (kernels.cpp:384-464), evaluated by every CTA ----
     const unsigned long long produced =
-        C == kClaimPlain && td ? (unsigned long long)snap.conv_count() : snap.produced();
-    const unsigned long long raw = td ? snap.raw() : produced;
+        (C == kClaimPlain && td) || red ? (unsigned long long)snap.conv_count() : snap.produced();
+    const unsigned long long raw = td && !red ? snap.raw() : produced;
     const unsigned long long edges = snap.edges();
     const unsigned long long pdeg = snap.degree();
     tl_mark(3);
@@ -1489,8 +1535,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
                      C == kClaimPlain ? p.bm[fcur ^ 1] : nullptr, p.force & kForceWideCompact);
       bar.sync(cnt);
       qlen = snap.conv_count();
-    } else if (C == kClaimBitmap && td && !next_td) {
-      // Entering bottom-up: the frontier bitmap from this level's distances.
+    } else if (C == kClaimBitmap && td && !next_td && !red) {
+      // Entering bottom-up: the frontier bitmap from this level's distances
+      // (a reduction-claim level left it in bm[fcur] already).
       front_from_dist(p.dist, depth + 1, p.bm[fcur], p.words, p.n, p.visited, p.init_mask);
       bar.sync();
     } else if (C == kClaimPlain && td && !next_td) {

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2503_00430_b200 as pb
+from paper_2503_00430_b200.parbfs import DeviceGraph
 from graphs import (from_edges, hand_suite, make_circulant, make_complete_bipartite,
                     make_clique, make_edgeless, make_path, make_star, random_graph)
 
@@ -356,6 +357,40 @@ def test_size_gated_paths_forced_on_small_graphs(force, port, monkeypatch):
             r = dg.bfs(s, pb.KernelConfig(variant=V.Hybrid, hybrid_threshold_fraction=0.001))
             assert np.array_equal(r.distances, want)
         g.release_device()
+
+
+@pytest.mark.parametrize("force", [0, 2])
+def test_reduction_claim_forced_on_small_graphs(force, port, monkeypatch):
+    # Top-down levels of >= 65536 frontier vertices claim with no-return reds
+    # and compact the next-frontier bitmap afterwards; forced onto every
+    # top-down level here (PBFS_RED_MINQ=1), with the narrow and the wide
+    # compaction. Distances must equal the oracle's, and per-level records
+    # the atomic-claim run's (phases, distinct sizes; raw == distinct).
+    monkeypatch.setenv("PBFS_RED_MINQ", "1")
+    monkeypatch.setenv("PBFS_FORCE_MODES", str(force))
+    graphs = [(pb.generate(pb.GeneratorSpec(pb.GeneratorKind.Kronecker, 15, 16, 7,
+                                            drop_self_loops=True)), 8),
+              (pb.generate(pb.GeneratorSpec(pb.GeneratorKind.UniformRandom, 14, 8, 2,
+                                            drop_self_loops=True)), 4),
+              (make_path(300), 8), (make_star(5000), 4), (random_graph(3000, 9000, 11), 8)]
+    for g, ob in graphs:
+        dg = DeviceGraph(g, 0, ob)
+        monkeypatch.setenv("PBFS_RED_MINQ", "0")
+        ref = DeviceGraph(g, 0, ob)
+        monkeypatch.setenv("PBFS_RED_MINQ", "1")
+        for s in [int(x) for x in pb.pick_sources(g, 3, 4)]:
+            want = port.bfs_serial(g.row_offsets, g.column_indices, s)
+            for v in (V.Hybrid, V.VisitedBitmapInline, V.HybridBeamer):
+                for kw in ({}, {"force_top_down_only": True}, {"hybrid_threshold_fraction": 0.5}):
+                    cfg = pb.KernelConfig(variant=v, **kw)
+                    r = dg.bfs(s, cfg)
+                    assert np.array_equal(r.distances, want), (v, s, kw)
+                    base = ref.bfs(s, cfg)
+                    assert ([(x.phase, x.distinct_size, x.frontier_size) for x in r.trace.records]
+                            == [(x.phase, x.distinct_size, x.frontier_size)
+                                for x in base.trace.records]), (v, s, kw)
+        ref.close()
+        dg.close()
 
 
 def test_time_run_checks_every_run(port):
