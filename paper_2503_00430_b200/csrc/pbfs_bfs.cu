@@ -425,7 +425,14 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   lc.numAttrs = nattr;
   if (p.obs) return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT, false, true>, p);
   if constexpr (C == kClaimBitmap) {
-    if (p.latency) return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT, true, false>, p);
+    if (p.latency) {
+      lc.dynamicSmemBytes = kLatSmem;
+      // Per launch: function attributes belong to the current device.
+      const cudaError_t ae = cudaFuncSetAttribute(bfs_latency<OffT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(kLatSmem));
+      if (ae != cudaSuccess) return ae;
+      return cudaLaunchKernelEx(&lc, bfs_latency<OffT>, p);
+    }
   }
   return cudaLaunchKernelEx(&lc, bfs_persistent<C, OffT>, p);
 }

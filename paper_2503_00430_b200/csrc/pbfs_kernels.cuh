@@ -174,6 +174,9 @@ struct alignas(128) Ctl {
   unsigned int bar_word;  // grid barrier: bit 31 flips once per completed barrier
   unsigned int pad0[31];
   LevelCnt cnt[4];
+  // Latency mode's multi-level rounds (latency_round): round r counts in
+  // row r & 3 (indices kLk*); a row is re-zeroed two rounds ahead.
+  alignas(128) unsigned long long latk[4][32];
   unsigned int overflow;  // PBFS_E_CAPACITY raised on device
   unsigned int levels;
   unsigned int bu_levels;
@@ -346,8 +349,9 @@ struct GridBarrier {
   VGrid vg = hw_grid();
   // `src` (optional, 64 B, 16 B aligned): thread 0 copies it into `snap`
   // after the barrier, so a CTA reads the level counters with one request
-  // instead of every thread polling the same L2 line.
-  __device__ __forceinline__ void sync(const void* src = nullptr) {
+  // instead of every thread polling the same L2 line; `src2` likewise into
+  // snap[8..15].
+  __device__ __forceinline__ void sync(const void* src = nullptr, const void* src2 = nullptr) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned nb = vg.cta == 0 ? 0x80000000u - (vg.ctas - 1) : 1u;
@@ -363,6 +367,30 @@ struct GridBarrier {
         snap[0] = a.x; snap[1] = a.y; snap[2] = b.x; snap[3] = b.y;
         snap[4] = c.x; snap[5] = c.y; snap[6] = d.x; snap[7] = d.y;
       }
+      if (src2) {
+        const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src2);
+        const ulonglong2 a = __ldcg(s2), b = __ldcg(s2 + 1), c = __ldcg(s2 + 2), d = __ldcg(s2 + 3);
+        snap[8] = a.x; snap[9] = a.y; snap[10] = b.x; snap[11] = b.y;
+        snap[12] = c.x; snap[13] = c.y; snap[14] = d.x; snap[15] = d.y;
+      }
+    }
+    __syncthreads();
+  }
+  // The barrier, then warp 0 copies the 32 u64 at src into snap[0..31].
+  __device__ __forceinline__ void sync32(const unsigned long long* src) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) {
+        const unsigned nb = vg.cta == 0 ? 0x80000000u - (vg.ctas - 1) : 1u;
+        unsigned old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;"
+                     : "=r"(old) : "l"(&ctl->bar_word), "r"(nb) : "memory");
+        while (((old ^ ld_relaxed(&ctl->bar_word)) & 0x80000000u) == 0) {
+        }
+      }
+      __syncwarp();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      snap[threadIdx.x] = __ldcg(src + threadIdx.x);
     }
     __syncthreads();
   }
@@ -889,6 +917,243 @@ __device__ void td_phase_latency(const Params<OffT>& p, uint32_t depth, const ui
   }
 }
 
+// ---- latency mode: several levels per grid barrier -----------------------------
+// The mesh's ~3900 levels are each one dependent chain (queue -> col ->
+// claim -> append) plus one grid barrier. A round runs kLatLevels levels per
+// barrier: the warp that wins a vertex at level d+j < d+kLatLevels expands
+// it itself right away (its row range is loaded in the shadow of the claim)
+// instead of handing it to the next level through the queue and a barrier;
+// only level d+kLatLevels goes to the next round's queue.
+//  * Claims are atomicMin on dist. Level d+1 is exact (every vertex at
+//    distance d+1 neighbours the complete level-d frontier); a claim at
+//    d+j, j >= 2, can be premature -- a slower warp may still reach the
+//    vertex at a lower level -- and is then lowered. The lowering warp owns
+//    the vertex at its true level and expands it; every vertex at distance
+//    d+j (j < kLatLevels) is therefore expanded at d+j exactly once within
+//    the round (its parent is, by induction), and distances are exact.
+//  * Bookkeeping keeps every per-level record equal to the level-synchronous
+//    one: distinct size = wins - lowerings at that level; edges examined =
+//    degrees expanded at that level minus those of vertices lowered from it
+//    (their expansion was wasted). A vertex lowered from d+kLatLevels stays
+//    in the next queue as a stale entry: expanded next round, every one of
+//    its claims fails (its neighbours hold <= d+kLatLevels by then), and its
+//    degree is taken off that level's count.
+// Grid-bipartite meshes make premature claims rare (a vertex's neighbours
+// sit one level up or down); the shortcut edges cause the few there are.
+#ifndef PBFS_LAT_LEVELS
+#define PBFS_LAT_LEVELS 5
+#endif
+constexpr int kLatLevels = PBFS_LAT_LEVELS;  // levels per grid barrier (1 = plain latency mode)
+static_assert(kLatLevels >= 1 && kLatLevels <= 6, "PBFS_LAT_LEVELS must be 1..6");
+// Dynamic shared memory of the latency kernel: kLatLevels buffers of 128
+// 16 B entries per warp (LatRound).
+constexpr size_t kLatSmem = kLatLevels >= 2 ? (size_t)kWarps * kLatLevels * 128 * 16 : 0;
+
+// Round counters (Ctl::latk[round & 3], one 256 B row): index
+//   kLkEdges0 (level d's expanded degrees), kLkCursor, kLkPush (next-queue
+//   appends), kLkWins + j, kLkLow + j (lowered from d+j), kLkLowDeg + j,
+//   kLkExp + j (degrees expanded at d+j), j = 1 .. kLatLevels.
+constexpr int kLkEdges0 = 0, kLkCursor = 1, kLkPush = 2, kLkWins = 4, kLkLow = 11, kLkLowDeg = 18,
+              kLkExp = 25;
+
+template <typename OffT>
+struct LatRound {
+  static constexpr int K = 4;          // edge slots per lane
+  // Entries per level buffer: one claim's winners, so each claim has a single
+  // drain / flush site and the nested expansion's code stays linear in
+  // kLatLevels. Buffers live in dynamic shared memory (kLatSmem per CTA).
+  static constexpr int kCap = 32 * K;
+  const Params<OffT>& p;
+  uint32_t d;
+  uint4* buf;                        // smem: level buffers 1 .. kLatLevels - 1, then the push buffer
+  uint4* qout;
+  unsigned long long* ctr;           // this round's counter row
+  WarpPush4 wp;
+  int lcount[kLatLevels + 1] = {};
+  // Per-lane tallies, reduced per warp at the end of the round.
+  unsigned long long edges0 = 0;
+  unsigned long long wins[kLatLevels + 1] = {}, low[kLatLevels + 1] = {}, lowdeg[kLatLevels + 1] = {},
+                     exp[kLatLevels + 1] = {};
+
+  // Level j's buffer (j = kLatLevels: the push buffer).
+  __device__ __forceinline__ uint4* level_buf(int j) { return buf + (j - 1) * kCap; }
+
+  // Claims at level d+J of K edge slots (okm = live slots).
+  template <int J>
+  __device__ __forceinline__ void claim(const uint32_t (&v)[K], uint32_t okm) {
+    const uint32_t nd = d + J;
+    uint32_t old[K];
+    OffT b0[K], b1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      old[k] = nd;
+      if ((okm >> k) & 1u) old[k] = atomicMin(&p.dist[v[k]], nd);
+      b0[k] = ld_stream(&p.rowptr[v[k]]);  // dead slots hold a valid id
+      b1[k] = ld_stream(&p.rowptr[v[k] + 1]);
+    }
+    uint32_t winmask = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool won = old[k] > nd;
+      winmask |= (uint32_t)won << k;
+      if constexpr (J < kLatLevels) {
+        // A premature claim at d+i (J < i <= kLatLevels) is lowered.
+        if (won && old[k] != kUnreached) {
+          const uint32_t i = old[k] - d;
+#pragma unroll
+          for (int q = J + 1; q <= kLatLevels; ++q) {
+            if (i == (uint32_t)q) {
+              ++low[q];
+              lowdeg[q] += (unsigned long long)(b1[k] - b0[k]);
+            }
+          }
+        }
+      }
+    }
+    wins[J] += __popc(winmask);
+    const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(winmask));
+    if (total == 0) return;
+    uint4* out;
+    int* cnt;
+    if constexpr (J < kLatLevels) {
+      if (lcount[J] + total > kCap) drain<J>();
+      out = level_buf(J);
+      cnt = &lcount[J];
+    } else {
+      if (wp.count + total > kCap) wp.flush(qout, &ctr[kLkPush], p.qcap, &p.ctl->overflow);
+      out = wp.buf;
+      cnt = &wp.count;
+    }
+    // Slot by slot: one ballot each, lanes in order.
+    int pos = *cnt;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool w = (winmask >> k) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, w);
+      if (w) {
+        const unsigned long long b = (unsigned long long)b0[k];
+        out[pos + __popc(m & lanemask_lt())] =
+            make_uint4(v[k], (uint32_t)(b1[k] - b0[k]), (uint32_t)b, (uint32_t)(b >> 32));
+      }
+      pos += __popc(m);
+    }
+    *cnt = pos;
+    __syncwarp();
+  }
+
+  // Warp-cooperative expansion of `count` row ranges {v, degree, beg lo, hi}
+  // (32 at a time, as td_phase_latency); every edge slot is claimed at d+J.
+  template <int J, class Load>
+  __device__ __forceinline__ void expand(unsigned long long count, Load&& load, unsigned long long& edges) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lane = lane_id();
+    for (unsigned long long base = 0; base < count; base += 32) {
+      uint32_t deg = 0;
+      unsigned long long beg = 0;
+      if (base + lane < count) {
+        const uint4 q = load(base + lane);
+        deg = q.y;
+        beg = (unsigned long long)q.z | ((unsigned long long)q.w << 32);
+      }
+      edges += deg;
+      uint32_t incl = deg;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (unsigned)o) incl += x;
+      }
+      const uint32_t total = __shfl_sync(FULL, incl, 31);
+      const uint32_t excl = incl - deg;
+      if (!total) continue;
+      const unsigned nz = __ballot_sync(FULL, deg != 0);
+      const unsigned long long b0 = __shfl_sync(FULL, beg, __ffs(nz) - 1);
+      for (uint32_t e0 = 0; e0 < total; e0 += 32 * K) {
+        uint32_t v[K];
+        uint32_t okm = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t e = e0 + 32 * k + lane;
+          int j = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t x = __shfl_sync(FULL, incl, j + step - 1);
+            if (x <= e) j += step;
+          }
+          const unsigned long long ob = __shfl_sync(FULL, beg, j);
+          const uint32_t oex = __shfl_sync(FULL, excl, j);
+          const bool ok = e < total;
+          okm |= (uint32_t)ok << k;
+          v[k] = ld_stream(&p.col[ok ? ob + (e - oex) : b0]);
+        }
+        claim<J>(v, okm);
+      }
+    }
+  }
+
+  // Expands local level buffer J (its vertices' claims are at d+J+1).
+  template <int J>
+  __device__ __forceinline__ void drain() {
+    if constexpr (J >= 1 && J < kLatLevels) {
+      __syncwarp();
+      const int n = lcount[J];
+      lcount[J] = 0;
+      // In place: this expansion's claims are at level J + 1 and append to
+      // buffer J + 1 (draining it, and deeper ones, when full), never to J.
+      uint4* lb = level_buf(J);
+      expand<J + 1>((unsigned long long)n, [&](unsigned long long i) { return lb[i]; }, exp[J]);
+      __syncwarp();
+    }
+  }
+};
+
+// One round (levels d .. d+kLatLevels-1) over the queue qin of qlen entries:
+// slices as td_phase_latency (adaptive width, dealt over the CTAs, then a
+// cursor), local levels drained in order at the end.
+template <typename OffT>
+__device__ void latency_round(const Params<OffT>& p, uint32_t d, const uint4* qin,
+                              unsigned long long qlen, uint4* qout, uint4* sbuf,
+                              unsigned long long* ctr) {
+  using LR = LatRound<OffT>;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = lane_id();
+  LR lr{p, d, sbuf, qout, ctr, WarpPush4{sbuf + (kLatLevels - 1) * LR::kCap, 0}};
+  const unsigned warps_total = gridDim.x * kWarps;
+  unsigned W = 32;
+  while (W > 1 && (unsigned long long)warps_total * (W / 2) >= qlen) W /= 2;
+  const unsigned gwi = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  unsigned long long base = (unsigned long long)gwi * W;
+  while (base < qlen) {
+    const unsigned long long n_here = qlen - base < W ? qlen - base : W;
+    lr.template expand<1>(n_here, [&](unsigned long long i) { return qin[base + i]; }, lr.edges0);
+    if (qlen <= (unsigned long long)warps_total * W) break;
+    unsigned int nb = 0;
+    if (lane == 0) nb = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLkCursor]), 32u);
+    base = (unsigned long long)warps_total * 32 + __shfl_sync(FULL, nb, 0);
+    W = 32;
+  }
+  // Local levels in order: draining level j only appends to levels > j.
+  if constexpr (kLatLevels >= 2) lr.template drain<1>();
+  if constexpr (kLatLevels >= 3) lr.template drain<2>();
+  if constexpr (kLatLevels >= 4) lr.template drain<3>();
+  if constexpr (kLatLevels >= 5) lr.template drain<4>();
+  if constexpr (kLatLevels >= 6) lr.template drain<5>();
+  lr.wp.flush(qout, &ctr[kLkPush], p.qcap, &p.ctl->overflow);
+  // Warp-reduced tallies into the round's row.
+  auto add = [&](int idx, unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    if (lane == 0 && x) atomicAdd(&ctr[idx], x);
+  };
+  add(kLkEdges0, lr.edges0);
+#pragma unroll
+  for (int j = 1; j <= kLatLevels; ++j) {
+    add(kLkWins + j, lr.wins[j]);
+    add(kLkLow + j, lr.low[j]);
+    add(kLkLowDeg + j, lr.lowdeg[j]);
+    if (j < kLatLevels) add(kLkExp + j, lr.exp[j]);
+  }
+}
+
 // Bottom-up over all vertices (kernels.cpp:340-382), per warp task of one
 // 32-word group (one visited word per lane), or of kBuSparseGroups groups
 // with all loads in flight when few vertices are left unvisited (settled
@@ -1289,11 +1554,12 @@ __device__ __forceinline__ void visited_front_from_dist(const uint32_t* __restri
 // kLat: latency mode (hub-free graphs run top-down only); kObs: observer
 // snapshots (test instrumentation). Separate instantiations, so neither
 // costs the general kernel registers.
-template <int C, typename OffT, bool kLat = false, bool kObs = false>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
+template <int C, typename OffT, bool kLat, bool kObs>
+__device__ __forceinline__ void bfs_traversal(const Params<OffT>& p) {
   __shared__ __align__(16) uint32_t s_list[kWarps][kListCap];  // BU id list / TD push buffer
+  extern __shared__ __align__(16) uint4 s_lat[];  // latency mode: per-warp level buffers (kLatSmem)
   __shared__ uint32_t s_found[kWarps][kGroupWords];
-  __shared__ unsigned long long s_snap[8];  // level-counter snapshot (GridBarrier)
+  __shared__ unsigned long long s_snap[32];  // level-counter snapshots (GridBarrier)
   const unsigned warp = threadIdx.x >> 5;
   const unsigned lane = lane_id();
   const unsigned long long tid = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
@@ -1334,6 +1600,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
         LevelCnt z{};
         ctl->cnt[s] = z;
       }
+      if (kLat) {
+        for (int s = 0; s < 4 * 32; ++s) (&ctl->latk[0][0])[s] = 0;
+      }
       ctl->overflow = 0;
       ctl->violations = 0;
       ctl->obs_count = 0;
@@ -1369,6 +1638,60 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
   // level touches no bitmap but `visited`, and the bitmap of its output is
   // built from dist only when bottom-up follows.
   uint32_t depth = 0;
+  if constexpr (kLat && kLatLevels >= 2) {
+    // ---- latency mode: kLatLevels levels per grid barrier (latency_round) ----
+
+    unsigned long long carry = 0;  // degree of last round's lowered vertices (stale queue entries)
+    for (unsigned r = 0;; ++r) {
+      unsigned long long* ctr = ctl->latk[r & 3];
+      if (leader) {
+        // Round r + 2's row: its last readers finished before round r - 1's barrier.
+        unsigned long long* z = ctl->latk[(r + 2) & 3];
+        for (int i = 0; i < 32; ++i) z[i] = 0;
+      }
+      latency_round(p, depth, p.lq[qcur], qlen, p.lq[qcur ^ 1],
+                    s_lat + warp * kLatLevels * LatRound<OffT>::kCap, ctr);
+      bar.sync32(ctr);
+      const unsigned long long* c = s_snap;
+      // Per-level distinct sizes and edge counts of the round (see LatRound).
+      unsigned long long dist_sz[kLatLevels + 1], edges[kLatLevels];
+      dist_sz[0] = cur_distinct;
+      edges[0] = c[kLkEdges0] - carry;
+      for (int j = 1; j <= kLatLevels; ++j) dist_sz[j] = c[kLkWins + j] - c[kLkLow + j];
+      for (int j = 1; j < kLatLevels; ++j) edges[j] = c[kLkExp + j] - c[kLkLowDeg + j];
+      int levels_here = 1;
+      while (levels_here < kLatLevels && dist_sz[levels_here] > 0) ++levels_here;
+      if (leader) {
+        const unsigned long long now = globaltimer();
+        const long long span = (long long)(now - t_start) / levels_here;  // one round, split evenly
+        for (int h = 0; h < levels_here && depth + h < p.rec_cap; ++h) {
+          pbfs_level rec;
+          rec.depth = depth + h;
+          rec.phase = PBFS_TOP_DOWN;
+          rec.frontier_size = rec.distinct_size = dist_sz[h];
+          rec.duplicate_count = 0;
+          rec.edges_examined = edges[h];
+          rec.flush_events = 0;
+          rec.elapsed_ns = span;
+          p.records[depth + h] = rec;
+        }
+        t_start = now;
+      }
+      for (int h = 0; h < levels_here; ++h) {
+        reached += dist_sz[h];
+        edges_total += edges[h];
+      }
+      if (levels_here < kLatLevels || dist_sz[kLatLevels] == 0) {
+        depth += levels_here - 1;  // the last level's index
+        break;
+      }
+      carry = c[kLkLowDeg + kLatLevels];
+      cur_distinct = dist_sz[kLatLevels];
+      qlen = c[kLkPush] < p.qcap ? c[kLkPush] : p.qcap;
+      qcur ^= 1;
+      depth += kLatLevels;
+    }
+  } else
   for (;; ++depth) {
     LevelCnt* cnt = &ctl->cnt[depth & 3];
     if (leader) {
@@ -1583,6 +1906,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<Of
     ctl->reached = reached;
     ctl->edges = edges_total;
   }
+}
+
+template <int C, typename OffT, bool kLat = false, bool kObs = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) bfs_persistent(Params<OffT> p) {
+  bfs_traversal<C, OffT, kLat, kObs>(p);
+}
+
+// Latency mode runs one CTA per SM (g->lat_grid): the round's nested
+// expansion gets the register file instead of spilling at the 3-CTA budget.
+template <typename OffT>
+__global__ void __launch_bounds__(kThreads, 1) bfs_latency(Params<OffT> p) {
+  bfs_traversal<kClaimBitmap, OffT, true, false>(p);
 }
 
 // Reached-component reduction over the last distance array (metric inputs).
