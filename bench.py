@@ -595,6 +595,11 @@ def run_single(args):
         f"{dg.info['block_threads']}, {dg.info['device_bytes']/2**30:.2f} GiB")
 
     sources = [int(s) for s in choose_sources(graph, dg, cfg, args.workload)]
+    # Latency mode (the library's choice for hub-free graphs run top-down only:
+    # every vertex's degree at or below the hub split threshold).
+    hub_deg = 256 if graph.edge_count >= (1 << 30) else 128
+    latency = bool(cfg.force_top_down_only) and dg.info["max_degree"] <= hub_deg \
+        and VARIANT in ("hybrid", "visited-inline", "hybrid-beamer")
     # A dedicated (non-default) stream: the kernel, the L2 flush and the
     # timing events must all be ordered on the same stream.
     stream = torch.cuda.Stream()
@@ -745,7 +750,9 @@ def run_single(args):
                                           "build_hash": tcap["build_hash"],
                                           "sources": tcap["sources"]} if tcap else None),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
-                     "kernel": "bfs_persistent (one cooperative launch per BFS)",
+                     "kernel": ("bfs_latency (one cooperative launch per BFS, several levels per "
+                                "grid barrier)" if latency else
+                                "bfs_persistent (one cooperative launch per BFS)"),
                      "bytes_model": "B_alg = 4*A_r + 2*W_off*N_r + 4*N per source; "
                                     "dram_frac = ncu dram bytes / (t x peak)"},
         "cpu_baseline": cpu,

@@ -42,7 +42,7 @@ def inner(args):
 def outer(args):
     log = os.path.join(ROOT, "gpurun_out", f"traffic_{args.workload}.csv")
     os.makedirs(os.path.dirname(log), exist_ok=True)
-    cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "-k", "regex:bfs_persistent",
+    cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "-k", "regex:bfs_(persistent|latency)",
            "--csv", "--log-file", log, sys.executable, os.path.abspath(__file__), "--inner",
            "--workload", args.workload, "--sources", str(args.sources), "--variant", args.variant]
     out = subprocess.run(cmd, capture_output=True, text=True)
@@ -70,7 +70,7 @@ def outer(args):
     total = sum(p["dram_bytes_read"] + p["dram_bytes_write"] for p in per)
     res = {
         "workload": args.workload, "variant": args.variant, "build_hash": bench.build_hash(),
-        "tool": f"ncu --metrics {METRICS} --clock-control none -k regex:bfs_persistent "
+        "tool": f"ncu --metrics {METRICS} --clock-control none -k regex:bfs_(persistent|latency) "
                 "(default cache control: caches flushed before each launch)",
         "sources": len(per),
         "dram_bytes_per_launch": total / len(per),
