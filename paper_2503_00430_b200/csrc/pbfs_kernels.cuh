@@ -72,6 +72,13 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_PRED_TD
 #define PBFS_PRED_TD 1  // predicated-off probes for dead top-down slots (A/B knob)
 #endif
+#ifndef PBFS_DIST_PROBE
+// dist probe of the CAS / plain-store top-down variants: 0 = L2 (ld.cg) for
+// every slot, 1 = through L1 (ld.ca; a set distance is final, a stale
+// kUnreached is settled by the CAS / is a benign same-value store), dead
+// slots predicated off; 2 = ld.cg, dead slots predicated off (A/B knob).
+#define PBFS_DIST_PROBE 0
+#endif
 #ifndef PBFS_TIMELINE
 #define PBFS_TIMELINE 0  // diagnostic per-level timeline in LevelRecord::flush_events
 #endif
@@ -511,6 +518,10 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
     } else if constexpr (C == kClaimBitmap && PBFS_PROBE == 2 && PBFS_PRED_TD) {
       // Dead slots issue no probe (read back as "visited").
       w[k] = ld_ca_if((okm >> k) & 1u, &p.visited[v[k] >> 5], 0xffffffffu);
+    } else if constexpr (C != kClaimBitmap && PBFS_DIST_PROBE == 1) {
+      w[k] = ld_ca_if((okm >> k) & 1u, &p.dist[v[k]], 0u);
+    } else if constexpr (C != kClaimBitmap && PBFS_DIST_PROBE == 2) {
+      w[k] = ld_cg_if((okm >> k) & 1u, &p.dist[v[k]], 0u);
     } else {
       w[k] = probe_word<C>(p, v[k]);
     }
