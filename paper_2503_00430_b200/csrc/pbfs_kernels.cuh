@@ -72,12 +72,24 @@ constexpr int kWarps = kThreads / 32;
 #ifndef PBFS_PRED_TD
 #define PBFS_PRED_TD 1  // predicated-off probes for dead top-down slots (A/B knob)
 #endif
-#ifndef PBFS_DIST_PROBE
 // dist probe of the CAS / plain-store top-down variants: 0 = L2 (ld.cg) for
 // every slot, 1 = through L1 (ld.ca; a set distance is final, a stale
 // kUnreached is settled by the CAS / is a benign same-value store), dead
-// slots predicated off; 2 = ld.cg, dead slots predicated off (A/B knob).
-#define PBFS_DIST_PROBE 0
+// slots predicated off; 2 = ld.cg, dead slots predicated off (A/B knobs).
+// RMAT-26 / ER-24 GTEPS (profiles/r02/ab.txt): CAS 0: 85.5 / 84.3,
+// 1: 90.7 / 83.1, 2: 91.5 / 86.4; plain 0: 91.3 / 88.4, 1: 105.1 / 89.4,
+// 2: 96.5 / 91.1.
+#ifndef PBFS_HOT_MODE
+#define PBFS_HOT_MODE 0  // visited-probe L1 policy by word index (ld_hot_if; 0 = plain ld.ca)
+#endif
+#ifndef PBFS_HOT_WORDS
+#define PBFS_HOT_WORDS 16384
+#endif
+#ifndef PBFS_CAS_PROBE
+#define PBFS_CAS_PROBE 2
+#endif
+#ifndef PBFS_PLAIN_PROBE
+#define PBFS_PLAIN_PROBE 1
 #endif
 #ifndef PBFS_TIMELINE
 #define PBFS_TIMELINE 0  // diagnostic per-level timeline in LevelRecord::flush_events
@@ -316,6 +328,34 @@ __device__ __forceinline__ uint32_t ld_ca_if(bool pred, const uint32_t* addr, ui
       : "r"((uint32_t)pred), "l"(addr));
   return dflt;
 }
+// Predicated visited probe with an L1 eviction policy by word index (A/B
+// knob PBFS_HOT_MODE / PBFS_HOT_WORDS): RMAT's hub core (the lowest ids) is
+// the L1-reusable part of the bitmap, the rest is a flood of one-touch lines.
+//   1: hot ld.ca,                 cold ld.L1::no_allocate
+//   2: hot ld.L1::evict_last,     cold ld.L1::evict_first
+//   3: hot ld.L1::evict_last,     cold ld.ca
+template <int M>
+__device__ __forceinline__ uint32_t ld_hot_if(bool pred, bool hot, const uint32_t* addr,
+                                              uint32_t dflt) {
+  const uint32_t h = (uint32_t)(pred && hot), c = (uint32_t)(pred && !hot);
+  if constexpr (M == 1) {
+    asm volatile(
+        "{\n\t.reg .pred h, c;\n\tsetp.ne.b32 h, %1, 0;\n\tsetp.ne.b32 c, %2, 0;\n\t"
+        "@h ld.global.ca.u32 %0, [%3];\n\t@c ld.global.L1::no_allocate.u32 %0, [%3];\n\t}"
+        : "+r"(dflt) : "r"(h), "r"(c), "l"(addr));
+  } else if constexpr (M == 2) {
+    asm volatile(
+        "{\n\t.reg .pred h, c;\n\tsetp.ne.b32 h, %1, 0;\n\tsetp.ne.b32 c, %2, 0;\n\t"
+        "@h ld.global.L1::evict_last.u32 %0, [%3];\n\t@c ld.global.L1::evict_first.u32 %0, [%3];\n\t}"
+        : "+r"(dflt) : "r"(h), "r"(c), "l"(addr));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred h, c;\n\tsetp.ne.b32 h, %1, 0;\n\tsetp.ne.b32 c, %2, 0;\n\t"
+        "@h ld.global.L1::evict_last.u32 %0, [%3];\n\t@c ld.global.ca.u32 %0, [%3];\n\t}"
+        : "+r"(dflt) : "r"(h), "r"(c), "l"(addr));
+  }
+  return dflt;
+}
 __device__ __forceinline__ void red_or_if(bool pred, uint32_t* addr, uint32_t val) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
@@ -515,12 +555,17 @@ __device__ __forceinline__ void claim_batch(const Params<OffT>& p, uint32_t nd,
   for (int k = 0; k < K; ++k) {
     if constexpr (C == kClaimBitmap && PBFS_PROBE == 3) {
       w[k] = 0;
+    } else if constexpr (C == kClaimBitmap && PBFS_PROBE == 2 && PBFS_PRED_TD && PBFS_HOT_MODE) {
+      w[k] = ld_hot_if<PBFS_HOT_MODE>((okm >> k) & 1u, (v[k] >> 5) < (uint32_t)PBFS_HOT_WORDS,
+                                      &p.visited[v[k] >> 5], 0xffffffffu);
     } else if constexpr (C == kClaimBitmap && PBFS_PROBE == 2 && PBFS_PRED_TD) {
       // Dead slots issue no probe (read back as "visited").
       w[k] = ld_ca_if((okm >> k) & 1u, &p.visited[v[k] >> 5], 0xffffffffu);
-    } else if constexpr (C != kClaimBitmap && PBFS_DIST_PROBE == 1) {
+    } else if constexpr (C != kClaimBitmap &&
+                         (C == kClaimCas ? PBFS_CAS_PROBE : PBFS_PLAIN_PROBE) == 1) {
       w[k] = ld_ca_if((okm >> k) & 1u, &p.dist[v[k]], 0u);
-    } else if constexpr (C != kClaimBitmap && PBFS_DIST_PROBE == 2) {
+    } else if constexpr (C != kClaimBitmap &&
+                         (C == kClaimCas ? PBFS_CAS_PROBE : PBFS_PLAIN_PROBE) == 2) {
       w[k] = ld_cg_if((okm >> k) & 1u, &p.dist[v[k]], 0u);
     } else {
       w[k] = probe_word<C>(p, v[k]);
