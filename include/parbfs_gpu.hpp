@@ -8,6 +8,8 @@
 //   parbfs::gpu::bfs(const CsrGraph&, VertexId, const KernelConfig&)
 //                                                      ~ kernels.hpp:34-75
 //   parbfs::gpu::kernel_fn()  -> parbfs::KernelFn      ~ timing.hpp:17-18
+//   ... and overloads taking a device list (std::vector<int32_t>): the graph
+//   partitioned over several GPUs (pbfs_graph_options.devices)
 // and rethrows C-ABI statuses as the reference exception classes
 // (types.hpp:25-68). The CsrGraph is borrowed zero-copy (its u64 offsets and
 // u32 columns are exactly pbfs_csr's layout); one device handle is cached per
@@ -125,10 +127,14 @@ class DeviceGraphCache {
     const long v = e ? std::strtol(e, nullptr, 10) : 4;
     return v > 0 ? static_cast<std::size_t>(v) : 1;
   }
-  Entry get(const CsrGraph& g, int device) {
+  Entry get(const CsrGraph& g, int device) { return get(g, std::vector<std::int32_t>{device}); }
+  // A device list of more than one entry partitions the graph over those GPUs
+  // (pbfs_graph_options.devices: the multi-partition engine, hybrid variant).
+  Entry get(const CsrGraph& g, const std::vector<std::int32_t>& devices) {
+    if (devices.empty()) throw ConfigError("empty device list");
     const Key key{static_cast<const void*>(&g), static_cast<const void*>(g.row_offsets.data()),
                   static_cast<const void*>(g.column_indices.data()), g.vertex_count, g.edge_count,
-                  device};
+                  devices};
     const std::uint64_t fp = fingerprint(g);
     std::lock_guard<std::mutex> lock(mu_);
     auto it = map_.find(key);
@@ -153,7 +159,11 @@ class DeviceGraphCache {
       }
       map_.erase(lru);
     }
-    pbfs_graph_options opt{device, 0};
+    pbfs_graph_options opt{devices[0], 0};
+    if (devices.size() > 1) {
+      opt.devices = devices.data();
+      opt.num_devices = static_cast<std::uint32_t>(devices.size());
+    }
     pbfs_graph* h = nullptr;
     throw_status(pbfs_graph_create(&csr, &opt, &h));
     Slot slot;
@@ -181,7 +191,8 @@ class DeviceGraphCache {
   }
 
  private:
-  using Key = std::tuple<const void*, const void*, const void*, std::uint64_t, std::uint64_t, int>;
+  using Key = std::tuple<const void*, const void*, const void*, std::uint64_t, std::uint64_t,
+                         std::vector<std::int32_t>>;
   struct Slot {
     Entry entry;
     std::uint64_t fp = 0;
@@ -279,16 +290,32 @@ inline BfsResult run_bfs(const CsrGraph& g, VertexId source, const KernelConfig&
   return bfs(g, source, effective, device);
 }
 
+// Several GPUs: the graph partitioned over `devices` (one partition per entry;
+// a repeated ordinal puts several partitions on one GPU), hybrid variant.
+inline BfsResult bfs(const CsrGraph& g, VertexId source, const KernelConfig& config,
+                     const std::vector<std::int32_t>& devices) {
+  validate(config);
+  const auto e = DeviceGraphCache::instance().get(g, devices);
+  return bfs_on(e.graph.get(), source, config, g.vertex_count);
+}
+inline BfsResult run_bfs(const CsrGraph& g, VertexId source, const KernelConfig& config,
+                         const GraphStats& stats, const std::vector<std::int32_t>& devices) {
+  KernelConfig effective = config;
+  if (stats.category == GraphCategory::LargeDiameter) effective.force_top_down_only = true;
+  return bfs(g, source, effective, devices);
+}
+
 // The plugin slot: time_run(graph, src, cfg, trials, warmups, gpu::kernel_fn()).
 // The stats come from the cached upload (computed once per graph).
-inline KernelFn kernel_fn(int device = 0) {
-  return [device](const CsrGraph& g, VertexId s, const KernelConfig& c) {
+inline KernelFn kernel_fn(const std::vector<std::int32_t>& devices) {
+  return [devices](const CsrGraph& g, VertexId s, const KernelConfig& c) {
     validate(c);
-    const auto e = DeviceGraphCache::instance().get(g, device);
+    const auto e = DeviceGraphCache::instance().get(g, devices);
     KernelConfig effective = c;
     if (e.stats.category == GraphCategory::LargeDiameter) effective.force_top_down_only = true;
     return bfs_on(e.graph.get(), s, effective, g.vertex_count);
   };
 }
+inline KernelFn kernel_fn(int device = 0) { return kernel_fn(std::vector<std::int32_t>{device}); }
 
 }  // namespace parbfs::gpu

@@ -11,6 +11,10 @@
 //   timerun         the reference's own oracle-checked time_run over
 //                   gpu::kernel_fn(); two equal-sized graphs rebuilt at one
 //                   address; the LevelObserver through the adapter.
+//   multi           the same calls over a device list (the graph partitioned
+//                   over {0,0} and {0,0,0}: loopback partitions on one GPU
+//                   through the multi-GPU exchange code): criterion-1 graphs
+//                   against bfs_serial, time_run over gpu::kernel_fn(devices).
 //   percall FILE N  plugin-slot e2e: read a CSR1 file into a CsrGraph,
 //                   call gpu::kernel_fn() once per source
 //                   (bfsbench pick_sources rule, seed 1) and print GTEPS per
@@ -132,6 +136,42 @@ int timerun() {
   return 0;
 }
 
+int multi() {
+  std::uint64_t runs = 0;
+  for (const std::vector<std::int32_t>& devs :
+       {std::vector<std::int32_t>{0, 0}, std::vector<std::int32_t>{0, 0, 0}}) {
+    for (int i = 0; i < 40; ++i) {
+      GeneratorSpec spec;
+      spec.kind = (i % 2 == 0) ? GeneratorKind::UniformRandom : GeneratorKind::Kronecker;
+      spec.scale = 4 + static_cast<std::uint32_t>(i % 9);
+      spec.edge_factor = 1 + static_cast<std::uint32_t>((i * 5) % 16);
+      spec.seed = 9000 + static_cast<std::uint64_t>(i);
+      const CsrGraph g = generate(spec);
+      const GraphStats stats = compute_stats(g);
+      KernelConfig cfg;
+      cfg.variant = KernelVariant::Hybrid;
+      for (const VertexId src : sources_of(g, 3, static_cast<std::uint64_t>(i))) {
+        const BfsResult got = gpu::run_bfs(g, src, cfg, stats, devs);
+        ++runs;
+        if (got.distances != bfs_serial(g, src)) {
+          std::printf("FAIL multi graph %d (%s) on %zu partitions source %u\n", i,
+                      to_string(spec).c_str(), devs.size(), src);
+          return 1;
+        }
+      }
+    }
+    const CsrGraph g = generate({GeneratorKind::Kronecker, 12, 16, 3});
+    KernelConfig cfg;
+    cfg.variant = KernelVariant::Hybrid;
+    const TimingReport rep = time_run(g, 0, cfg, 3, 1, gpu::kernel_fn(devs));
+    std::printf("time_run over %zu partitions: median %lld ns\n", devs.size(),
+                static_cast<long long>(rep.median.count()));
+  }
+  std::printf("OK multi %llu runs through gpu::run_bfs over device lists\n",
+              static_cast<unsigned long long>(runs));
+  return 0;
+}
+
 // The CSR1 file (graph_io.hpp layout) read straight into a CsrGraph: the
 // reference's own load_binary_csr parses it element by element (minutes at
 // RMAT-26). The file comes from the symmetric generator.
@@ -193,11 +233,12 @@ int main(int argc, char** argv) {
   try {
     if (mode == "criterion1") return criterion1();
     if (mode == "timerun") return timerun();
+    if (mode == "multi") return multi();
     if (mode == "percall" && argc > 3) return percall(argv[2], std::strtoull(argv[3], nullptr, 10));
   } catch (const Error& e) {
     std::printf("ERROR %s\n", e.what());
     return std::strstr(e.what(), "no CUDA device") ? 3 : 1;
   }
-  std::printf("usage: adapter_check criterion1|timerun|percall FILE N\n");
+  std::printf("usage: adapter_check criterion1|timerun|multi|percall FILE N\n");
   return 2;
 }

@@ -63,7 +63,7 @@ ADAPTER = os.path.join(ROOT, "oracle", "_ref", "adapter_check")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["criterion1", "timerun"])
+@pytest.mark.parametrize("mode", ["criterion1", "timerun", "multi"])
 def test_reference_drives_the_b200_through_the_cpp_adapter(mode):
     # tests/cpp/adapter_check.cpp, prebuilt here against the unmodified
     # reference headers (make -C oracle adapter) and shipped with the repo:
