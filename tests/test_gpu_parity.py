@@ -359,12 +359,12 @@ def test_size_gated_paths_forced_on_small_graphs(force, port, monkeypatch):
         g.release_device()
 
 
-@pytest.mark.parametrize("force", [0, 2])
+@pytest.mark.parametrize("force", [0, 2, 4])
 def test_reduction_claim_forced_on_small_graphs(force, port, monkeypatch):
     # Top-down levels of >= 65536 frontier vertices claim with no-return reds
     # and compact the next-frontier bitmap afterwards; forced onto every
     # top-down level here (PBFS_RED_MINQ=1), with the narrow and the wide
-    # compaction. Distances must equal the oracle's, and per-level records
+    # compaction and the >= 2^30-arc hub split (1024-edge items). Distances must equal the oracle's, and per-level records
     # the atomic-claim run's (phases, distinct sizes; raw == distinct).
     monkeypatch.setenv("PBFS_RED_MINQ", "1")
     monkeypatch.setenv("PBFS_FORCE_MODES", str(force))
