@@ -801,7 +801,15 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
       g->persist_bytes = want;
     }
   }
-  g->red_minq = kRedMinQ;
+  // Reduction claim: only where visited + both frontier bitmaps fit the
+  // persisting-L2 set-aside. Its reds go to two bitmaps instead of one, and
+  // on RMAT-28 (96 MB of bitmaps against 79 MB) they miss L2 and cost more
+  // than the claim round trips they save: 423 GTEPS with it, 448 without
+  // (RMAT-26, 25 MB: 491 with, 476 without; profiles/r02/ab.txt).
+  const size_t red_fit = prop.persistingL2CacheMaxSize > 0
+                             ? static_cast<size_t>(prop.persistingL2CacheMaxSize)
+                             : (64u << 20);
+  g->red_minq = 3 * wbytes <= red_fit ? kRedMinQ : 0;
   if (const char* q = std::getenv("PBFS_RED_MINQ")) g->red_minq = static_cast<uint32_t>(std::strtoul(q, nullptr, 0));
   cudaSetDevice(prev);
   *out = g;

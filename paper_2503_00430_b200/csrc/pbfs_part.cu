@@ -549,13 +549,6 @@ pbfs_status build_partition(pbfs_part* g, const OffT* rowptr, const uint32_t* co
   return PBFS_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-}  // extern "C"
-
-namespace {
 pbfs_status part_create_impl(uint64_t n, bool symmetric, int device, const void* rowptr,
                              const uint32_t* col, uint32_t offb, const pbfs_part_options* opt,
                              pbfs_part** out);
