@@ -151,7 +151,9 @@ class Widener {
         j.dst[k] = x == 0xFFFF ? 0xFFFFFFFFu : x;
       }
     };
-    while (i < e && (reinterpret_cast<uintptr_t>(j.dst + i) & 15)) scalar(i++);
+    while (i < e && (reinterpret_cast<uintptr_t>(j.dst + i) & 63)) scalar(i++);
+    // Whole-line stores where the host has AVX-512 (pbfs_graph.cpp).
+    if (j.width == 1 && i < e && widen_codes_avx512(static_cast<const uint8_t*>(j.src), j.dst, i, e)) return;
     const __m128i ones = _mm_set1_epi32(-1);
     if (j.width == 1) {
       const uint8_t* s = static_cast<const uint8_t*>(j.src);

@@ -5,6 +5,7 @@
 // multi-GB graphs: no O(m log m) global sort, no value-initialised buffers,
 // the mt19937_64 stream cut into chunks by jump-ahead (pbfs_mt64.h) and
 // generated on every host thread.
+#include <immintrin.h>
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -477,6 +478,36 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
   out->symmetric = symmetrize ? true : is_symmetric(*out, threads);
   return PBFS_OK;
 }
+
+#if defined(__x86_64__) && defined(__GNUC__)
+// One 64 B line of output per 16 codes: vpmovzxbd, the unreached code patched
+// to all-ones under a mask, one vmovntdq. A line written by a single store
+// never leaves a write-combining buffer half filled, which matters when the
+// inbound DMA of the next transfer shares the memory system.
+__attribute__((target("avx512f,avx512bw,avx512vl")))
+static void widen_codes_avx512_impl(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e) {
+  uint64_t i = b;
+  const __m512i ones = _mm512_set1_epi32(-1);
+  const __m128i ff = _mm_set1_epi8(static_cast<char>(0xFF));
+  for (; i + 16 <= e; i += 16) {
+    const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __mmask16 un = _mm_cmpeq_epi8_mask(x, ff);
+    const __m512i w = _mm512_mask_mov_epi32(_mm512_cvtepu8_epi32(x), un, ones);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), w);
+  }
+  for (; i < e; ++i) dst[i] = src[i] == 0xFF ? 0xFFFFFFFFu : src[i];
+  _mm_sfence();
+}
+bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e) {
+  static const bool have = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+                           __builtin_cpu_supports("avx512vl") && !std::getenv("PBFS_NO_AVX512");
+  if (!have || (reinterpret_cast<uintptr_t>(dst + b) & 63)) return false;
+  widen_codes_avx512_impl(src, dst, b, e);
+  return true;
+}
+#else
+bool widen_codes_avx512(const uint8_t*, uint32_t*, uint64_t, uint64_t) { return false; }
+#endif
 
 pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads) {
   if (c->vertex_count > 0x7fffffffULL) {

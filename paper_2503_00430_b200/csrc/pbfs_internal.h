@@ -51,6 +51,12 @@ inline uint64_t csr_offset(const pbfs_csr* c, uint64_t i) {
                               : static_cast<const uint32_t*>(c->row_offsets)[i];
 }
 
+// 1 B / vertex level codes (0xFF = unreached) -> uint32 distances for entries
+// [b, e), with whole-cache-line non-temporal stores where the host has
+// AVX-512 (pbfs_graph.cpp; runtime dispatch). Returns false when the host
+// lacks it (the caller's SSE2 loop runs instead). dst + b must be 64 B aligned.
+bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e);
+
 // Structural validation of a borrowed CSR (validate_csr, csr_graph.cpp:68-113).
 pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads);
 
