@@ -758,7 +758,7 @@ def run_single(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
                 "h2d_bytes_per_step": 4 * NUM_SOURCES,
-                "d2h_bytes_per_step": int(sum(widths)) * n,
+                "d2h_bytes_per_step": int(sum(widths) * n),
                 "note": "pbfs_bfs_batch C-ABI call over the 64 sources: every distance array "
                         "copied to pinned host memory (two rotating buffers) while the next "
                         "traversal runs -- from 2^25 vertices as 1 B/vertex level codes "

@@ -113,8 +113,9 @@ typedef struct pbfs_run_info {
   uint64_t same_value_violations; /* under validate_same_value_stores */
   uint64_t edges_examined;
   float device_ms;                /* CUDA-event time of the traversal kernel */
-  uint32_t transfer_width;        /* pbfs_bfs_batch: bytes per vertex moved device->host
-                                     (1 or 2 when packed, else 4); 0 elsewhere */
+  uint32_t transfer_width;        /* pbfs_bfs_batch: bytes per vertex moved device->host,
+                                     rounded up (1 or 2 when packed -- 4-bit codes, used
+                                     below 15 levels, report 1 -- else 4); 0 elsewhere */
 } pbfs_run_info;
 
 typedef struct pbfs_graph_options {

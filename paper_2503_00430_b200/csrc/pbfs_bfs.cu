@@ -63,7 +63,7 @@ class Widener {
     const void* src = nullptr;
     uint32_t* dst = nullptr;
     uint64_t n = 0;
-    uint32_t width = 0;  // 0 = nothing to widen (bookkeeping only)
+    uint32_t width = 0;  // code width in BITS (4, 8 or 16); 0 = nothing to widen (bookkeeping only)
     uint64_t id = 0;
     Widener* owner = nullptr;
   };
@@ -141,9 +141,12 @@ class Widener {
   // all-ones mask turns 0xFF / 0xFFFF into 0xFFFFFFFF and zero-extends the
   // rest.
   static void widen(const Job& j, uint64_t b, uint64_t e) {
-    uint64_t i = b;
+    uint64_t i = b;  // a multiple of 64 (even: nibble codes pair up)
     auto scalar = [&](uint64_t k) {
-      if (j.width == 1) {
+      if (j.width == 4) {
+        const uint32_t x = (static_cast<const uint8_t*>(j.src)[k >> 1] >> ((k & 1) * 4)) & 0xFu;
+        j.dst[k] = x == 0xF ? 0xFFFFFFFFu : x;
+      } else if (j.width == 8) {
         const uint8_t x = static_cast<const uint8_t*>(j.src)[k];
         j.dst[k] = x == 0xFF ? 0xFFFFFFFFu : x;
       } else {
@@ -151,22 +154,36 @@ class Widener {
         j.dst[k] = x == 0xFFFF ? 0xFFFFFFFFu : x;
       }
     };
-    while (i < e && (reinterpret_cast<uintptr_t>(j.dst + i) & 63)) scalar(i++);
+    while (i < e && ((reinterpret_cast<uintptr_t>(j.dst + i) & 63) || (i & 1))) scalar(i++);
     // Whole-line stores where the host has AVX-512 (pbfs_graph.cpp).
-    if (j.width == 1 && i < e && widen_codes_avx512(static_cast<const uint8_t*>(j.src), j.dst, i, e)) return;
+    if (j.width <= 8 && i < e &&
+        widen_codes_avx512(static_cast<const uint8_t*>(j.src), j.dst, i, e, j.width)) return;
     const __m128i ones = _mm_set1_epi32(-1);
-    if (j.width == 1) {
+    // 16 one-byte codes x (m = their unreached mask) -> 16 uint32 at d.
+    auto expand16 = [&](__m128i x, __m128i m, __m128i* d) {
+      const __m128i lo = _mm_unpacklo_epi8(x, m), hi = _mm_unpackhi_epi8(x, m);
+      const __m128i mlo = _mm_unpacklo_epi8(m, m), mhi = _mm_unpackhi_epi8(m, m);
+      _mm_stream_si128(d + 0, _mm_unpacklo_epi16(lo, mlo));
+      _mm_stream_si128(d + 1, _mm_unpackhi_epi16(lo, mlo));
+      _mm_stream_si128(d + 2, _mm_unpacklo_epi16(hi, mhi));
+      _mm_stream_si128(d + 3, _mm_unpackhi_epi16(hi, mhi));
+    };
+    if (j.width == 4) {
+      const uint8_t* s = static_cast<const uint8_t*>(j.src);
+      const __m128i nib = _mm_set1_epi8(0x0F);
+      for (; i + 16 <= e; i += 16) {
+        const __m128i x = _mm_loadl_epi64(reinterpret_cast<const __m128i*>(s + (i >> 1)));
+        const __m128i lo = _mm_and_si128(x, nib), hi = _mm_and_si128(_mm_srli_epi16(x, 4), nib);
+        const __m128i y = _mm_unpacklo_epi8(lo, hi);  // vertex order: even = low nibble
+        // 0x0F -> 0xFF under its own mask, so the byte expansion's all-ones rule applies
+        const __m128i m = _mm_cmpeq_epi8(y, nib);
+        expand16(_mm_or_si128(y, m), m, reinterpret_cast<__m128i*>(j.dst + i));
+      }
+    } else if (j.width == 8) {
       const uint8_t* s = static_cast<const uint8_t*>(j.src);
       for (; i + 16 <= e; i += 16) {
         const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
-        const __m128i m = _mm_cmpeq_epi8(x, ones);
-        const __m128i lo = _mm_unpacklo_epi8(x, m), hi = _mm_unpackhi_epi8(x, m);
-        const __m128i mlo = _mm_unpacklo_epi8(m, m), mhi = _mm_unpackhi_epi8(m, m);
-        __m128i* d = reinterpret_cast<__m128i*>(j.dst + i);
-        _mm_stream_si128(d + 0, _mm_unpacklo_epi16(lo, mlo));
-        _mm_stream_si128(d + 1, _mm_unpackhi_epi16(lo, mlo));
-        _mm_stream_si128(d + 2, _mm_unpacklo_epi16(hi, mhi));
-        _mm_stream_si128(d + 3, _mm_unpackhi_epi16(hi, mhi));
+        expand16(x, _mm_cmpeq_epi8(x, ones), reinterpret_cast<__m128i*>(j.dst + i));
       }
     } else {
       const uint16_t* s = static_cast<const uint16_t*>(j.src);
@@ -255,6 +272,7 @@ struct pbfs_graph {
   uint32_t ctl_host_cap = 0;
   std::vector<cudaEvent_t> run_ev;  // per-source start/end events (2 per source)
   uint32_t red_minq = 0;  // reduction-claim frontier length (bfs_persistent), 0 = off
+  uint32_t pack_min_bits = 4;  // narrowest packed transfer code (PBFS_PACK_MIN_BITS=8: no 4-bit codes)
 };
 
 namespace {
@@ -404,6 +422,7 @@ cudaError_t launch_typed(pbfs_graph* g, uint32_t source, const pbfs_config* cfg,
   p.alpha = cfg->alpha;
   p.beta = cfg->beta;
   p.red_minq = g->red_minq;
+  p.pack_min_bits = g->pack_min_bits;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(p.latency ? g->lat_grid : g->grid);
   lc.blockDim = dim3(kThreads);
@@ -813,6 +832,7 @@ pbfs_status pbfs_graph_create(const pbfs_csr* csr, const pbfs_graph_options* opt
                              : (64u << 20);
   g->red_minq = 3 * wbytes <= red_fit ? kRedMinQ : 0;
   if (const char* q = std::getenv("PBFS_RED_MINQ")) g->red_minq = static_cast<uint32_t>(std::strtoul(q, nullptr, 0));
+  if (const char* b = std::getenv("PBFS_PACK_MIN_BITS")) g->pack_min_bits = std::atoi(b) >= 8 ? 8u : 4u;
   cudaSetDevice(prev);
   *out = g;
   return PBFS_OK;
@@ -892,12 +912,13 @@ pbfs_status pbfs_bfs_locked(pbfs_graph* g, uint32_t source, const pbfs_config* c
     return fail(PBFS_E_CAPACITY, "dense frontier overflow");
   }
   if (dist_host) {
-    const uint32_t width = packed ? pack_width(ctl.levels) : 4u;
-    if (width < 4) {
-      PBFS_CUDA(cudaMemcpy(g->stage1, g->pack1, g->n * width, cudaMemcpyDeviceToHost), "read distances");
+    const uint32_t bits = packed ? pack_bits(ctl.levels, g->pack_min_bits) : 32u;
+    if (bits < 32) {
+      PBFS_CUDA(cudaMemcpy(g->stage1, g->pack1, packed_bytes(g->n, bits), cudaMemcpyDeviceToHost),
+                "read distances");
       Widener& wd = *g->widener;
       wd.reset();
-      Widener::Job job{g->stage1, dist_host, g->n, width, 0, &wd};
+      Widener::Job job{g->stage1, dist_host, g->n, bits, 0, &wd};
       wd.submit(job);
       wd.wait(0);
     } else {
@@ -1044,9 +1065,10 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     ce = cudaEventSynchronize(g->kern_done[slot]);
     if (ce != cudaSuccess) return ce;
     const Ctl& c = g->ctl_host[j];
-    const uint32_t width = packed ? pack_width(c.levels) : 4u;
+    const uint32_t bits = packed ? pack_bits(c.levels, g->pack_min_bits) : 32u;
+    const uint32_t width = bits < 32 ? 1u : 4u;  // below: < 4 = codes + widening, 4 = the plain copy
     Widener::Job& job = jobs[j];
-    job = Widener::Job{g->stage[slot], dist_host[j], n, width < 4 ? width : 0, j, &wd};
+    job = Widener::Job{g->stage[slot], dist_host[j], n, bits < 32 ? bits : 0, j, &wd};
     // stage[slot] was last read by job j-S. dist_host[j] may alias an earlier
     // output (rotating buffers): the pool runs jobs in order, so only a DMA
     // straight into dist_host (the 4 B fallback) waits for that job.
@@ -1057,7 +1079,7 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
     last_use[dist_host[j]] = j;
     if ((ce = cudaStreamWaitEvent(g->copy_stream, g->kern_done[slot], 0)) != cudaSuccess) return ce;
     if (width < 4) {
-      ce = cudaMemcpyAsync(g->stage[slot], g->pack[slot], n * width, cudaMemcpyDeviceToHost,
+      ce = cudaMemcpyAsync(g->stage[slot], g->pack[slot], packed_bytes(n, bits), cudaMemcpyDeviceToHost,
                            g->copy_stream);
     } else {
       reads_dist[j] = 1;  // > 65534 levels: the full 4 B copy of the dist buffer

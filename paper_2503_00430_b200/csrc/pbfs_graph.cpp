@@ -485,28 +485,47 @@ pbfs_status build_csr_impl(const uint32_t* pairs, uint64_t npairs, uint64_t n, b
 // never leaves a write-combining buffer half filled, which matters when the
 // inbound DMA of the next transfer shares the memory system.
 __attribute__((target("avx512f,avx512bw,avx512vl")))
-static void widen_codes_avx512_impl(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e) {
+static void widen_codes_avx512_impl(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e,
+                                    uint32_t bits) {
   uint64_t i = b;
   const __m512i ones = _mm512_set1_epi32(-1);
-  const __m128i ff = _mm_set1_epi8(static_cast<char>(0xFF));
-  for (; i + 16 <= e; i += 16) {
-    const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
-    const __mmask16 un = _mm_cmpeq_epi8_mask(x, ff);
-    const __m512i w = _mm512_mask_mov_epi32(_mm512_cvtepu8_epi32(x), un, ones);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), w);
+  if (bits == 4) {
+    const __m128i nib = _mm_set1_epi8(0x0F);
+    for (; i + 16 <= e; i += 16) {
+      const __m128i x = _mm_loadl_epi64(reinterpret_cast<const __m128i*>(src + (i >> 1)));
+      const __m128i lo = _mm_and_si128(x, nib), hi = _mm_and_si128(_mm_srli_epi16(x, 4), nib);
+      const __m128i y = _mm_unpacklo_epi8(lo, hi);  // vertex order: even = low nibble
+      const __mmask16 un = _mm_cmpeq_epi8_mask(y, nib);
+      _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i),
+                          _mm512_mask_mov_epi32(_mm512_cvtepu8_epi32(y), un, ones));
+    }
+    for (; i < e; ++i) {
+      const uint32_t c = (src[i >> 1] >> ((i & 1) * 4)) & 0xFu;
+      dst[i] = c == 0xF ? 0xFFFFFFFFu : c;
+    }
+  } else {
+    const __m128i ff = _mm_set1_epi8(static_cast<char>(0xFF));
+    for (; i + 16 <= e; i += 16) {
+      const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+      const __mmask16 un = _mm_cmpeq_epi8_mask(x, ff);
+      _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i),
+                          _mm512_mask_mov_epi32(_mm512_cvtepu8_epi32(x), un, ones));
+    }
+    for (; i < e; ++i) dst[i] = src[i] == 0xFF ? 0xFFFFFFFFu : src[i];
   }
-  for (; i < e; ++i) dst[i] = src[i] == 0xFF ? 0xFFFFFFFFu : src[i];
   _mm_sfence();
 }
-bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e) {
+bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e, uint32_t bits) {
   static const bool have = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
                            __builtin_cpu_supports("avx512vl") && !std::getenv("PBFS_NO_AVX512");
-  if (!have || (reinterpret_cast<uintptr_t>(dst + b) & 63)) return false;
-  widen_codes_avx512_impl(src, dst, b, e);
+  if (!have || (bits != 4 && bits != 8) || (reinterpret_cast<uintptr_t>(dst + b) & 63) || (b & 1)) {
+    return false;
+  }
+  widen_codes_avx512_impl(src, dst, b, e, bits);
   return true;
 }
 #else
-bool widen_codes_avx512(const uint8_t*, uint32_t*, uint64_t, uint64_t) { return false; }
+bool widen_codes_avx512(const uint8_t*, uint32_t*, uint64_t, uint64_t, uint32_t) { return false; }
 #endif
 
 pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads) {

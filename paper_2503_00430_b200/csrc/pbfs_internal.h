@@ -51,11 +51,13 @@ inline uint64_t csr_offset(const pbfs_csr* c, uint64_t i) {
                               : static_cast<const uint32_t*>(c->row_offsets)[i];
 }
 
-// 1 B / vertex level codes (0xFF = unreached) -> uint32 distances for entries
-// [b, e), with whole-cache-line non-temporal stores where the host has
-// AVX-512 (pbfs_graph.cpp; runtime dispatch). Returns false when the host
-// lacks it (the caller's SSE2 loop runs instead). dst + b must be 64 B aligned.
-bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e);
+// Level codes of `bits` = 4 (vertex v in byte v / 2, low nibble for even v;
+// 0xF = unreached) or 8 (0xFF = unreached) bits per vertex -> uint32 distances
+// for entries [b, e), with whole-cache-line non-temporal stores where the host
+// has AVX-512 (pbfs_graph.cpp; runtime dispatch). Returns false when the host
+// lacks it (the caller's SSE2 loop runs instead). dst + b must be 64 B aligned
+// and b even.
+bool widen_codes_avx512(const uint8_t* src, uint32_t* dst, uint64_t b, uint64_t e, uint32_t bits);
 
 // Structural validation of a borrowed CSR (validate_csr, csr_graph.cpp:68-113).
 pbfs_status validate_csr_view(const pbfs_csr* c, unsigned threads);

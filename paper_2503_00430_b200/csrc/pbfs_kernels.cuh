@@ -205,10 +205,22 @@ struct alignas(128) Ctl {
   unsigned long long edges;
 };
 
-// Bytes per vertex of the packed host transfer for a traversal of `levels`
-// levels (distances 0 .. levels-1, plus the unreached marker); 4 = no pack.
-__host__ __device__ __forceinline__ uint32_t pack_width(uint32_t levels) {
-  return levels < 0xFF ? 1u : levels < 0xFFFF ? 2u : 4u;
+// Bits per vertex of the packed host transfer for a traversal of `levels`
+// levels (distances 0 .. levels-1, plus the all-ones unreached code): 4-bit
+// codes when every level fits a nibble (RMAT: 7-9 levels), then 1 or 2 bytes;
+// 32 = no pack. pack_width is the same in whole bytes, rounded up (what
+// pbfs_run_info::transfer_width reports).
+__host__ __device__ __forceinline__ uint32_t pack_bits(uint32_t levels, uint32_t min_bits = 4) {
+  const uint32_t b = levels < 0xF ? 4u : levels < 0xFF ? 8u : levels < 0xFFFF ? 16u : 32u;
+  return b < min_bits ? min_bits : b;  // min_bits = 8: no nibble codes (PBFS_PACK_MIN_BITS, A/B knob)
+}
+__host__ __device__ __forceinline__ uint32_t pack_width(uint32_t levels, uint32_t min_bits = 4) {
+  const uint32_t b = pack_bits(levels, min_bits);
+  return b < 8 ? 1u : b / 8;
+}
+// Bytes of a packed copy of n distances (whole 16 B vectors for the nibble codes).
+__host__ __device__ __forceinline__ unsigned long long packed_bytes(unsigned long long n, uint32_t bits) {
+  return bits == 4 ? ((n + 31) / 32) * 16 : n * (bits / 8);
 }
 
 struct HeavyItem {
@@ -241,7 +253,8 @@ struct Params {
   uint32_t chunk_log2;  // log2 of edges per heavy item
   uint32_t small_chunks;  // heavy_cap covers kSmallChunkLog2 items on small frontiers
   uint32_t force;         // kForce* test hooks (PBFS_FORCE_MODES at graph creation)
-  void* pack;             // optional: narrow copy of dist for the host transfer (see pack_width)
+  void* pack;             // optional: narrow copy of dist for the host transfer (see pack_bits)
+  uint32_t pack_min_bits = 4;
   // Latency mode (deep, hub-free graphs run top-down only, e.g. config 3's
   // mesh): 16 B queue entries {v, degree, row offset lo, hi}, see td_phase_latency.
   uint4* lq[2];
@@ -1935,9 +1948,24 @@ __device__ __forceinline__ void bfs_traversal(const Params<OffT>& p) {
   // when every level fits (0xFF = unreached), else 2 B. No barrier needed:
   // the loop ended on one, after the last level's stores.
   if (p.pack) {
-    const uint32_t width = pack_width(depth + 1);
+    const uint32_t bits = pack_bits(depth + 1, p.pack_min_bits);
+    const uint32_t width = bits / 8;
     const uint4* d4 = reinterpret_cast<const uint4*>(p.dist);
-    if (width == 1) {
+    if (bits == 4) {
+      // 32 vertices per 16 B: vertex v in byte v / 2, low nibble for even v.
+      uint4* o = reinterpret_cast<uint4*>(p.pack);
+      for (unsigned long long i = tid; i < (p.n + 31) / 32; i += nthreads) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a = __ldcs(d4 + 8 * i + 2 * q);  // dist is padded to 32 entries
+          const uint4 b = __ldcs(d4 + 8 * i + 2 * q + 1);
+          w[q] = (a.x & 0xF) | (a.y & 0xF) << 4 | (a.z & 0xF) << 8 | (a.w & 0xF) << 12 |
+                 (b.x & 0xF) << 16 | (b.y & 0xF) << 20 | (b.z & 0xF) << 24 | (b.w & 0xF) << 28;
+        }
+        o[i] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else if (width == 1) {
       uint4* o = reinterpret_cast<uint4*>(p.pack);
       for (unsigned long long i = tid; i < (p.n + 15) / 16; i += nthreads) {
         uint32_t w[4];

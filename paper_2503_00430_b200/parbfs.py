@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import os
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -668,7 +669,8 @@ class DeviceGraph:
         """pbfs_bfs_batch: traversal i+1 overlaps the host copy of distances i.
         `outs[i]` receives source i's distances (entries may repeat, e.g. two
         rotating pinned buffers). Returns per-source device ms; `widths`, if
-        given, receives the bytes per vertex each transfer moved."""
+        given, receives the bytes per vertex each transfer moved (0.5 for
+        4-bit codes)."""
         srcs = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
         k = int(srcs.size)
         if len(outs) != k:
@@ -682,7 +684,11 @@ class DeviceGraph:
         _check(lib.pbfs_bfs_batch(self.h, srcs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
                                   k, ctypes.byref(c), ptrs, infos))
         if widths is not None:
-            widths[:] = [int(infos[i].transfer_width) for i in range(k)]
+            # transfer_width is in whole bytes, rounded up: a packed traversal
+            # of fewer than 15 levels moves 4-bit codes (pack_bits).
+            nibble = os.environ.get("PBFS_PACK_MIN_BITS", "4") != "8"
+            widths[:] = [0.5 if nibble and infos[i].transfer_width == 1 and infos[i].levels < 15
+                         else int(infos[i].transfer_width) for i in range(k)]
         return [float(infos[i].device_ms) for i in range(k)]
 
     def bfs_async(self, source: int, config: KernelConfig, stream: int = 0) -> None:

@@ -302,7 +302,8 @@ def test_batch_api_overlapped_copies(force, slots, port, monkeypatch):
         widths = []
         ms = dg.bfs_batch(srcs, cfg, outs, widths)
         assert len(ms) == len(srcs) and all(t > 0 for t in ms)
-        assert widths == [1 if force == "8" else 4] * len(srcs)
+        # packed: < 15 levels here, so 4-bit codes
+        assert widths == [0.5 if force == "8" else 4] * len(srcs)
         for s, o in zip(srcs, outs):
             assert np.array_equal(o, want[s])
         # the handle's device distances are the last source's
@@ -320,7 +321,8 @@ def test_batch_api_overlapped_copies(force, slots, port, monkeypatch):
                      [np.empty(g.vertex_count, np.uint32)] * 2)
     # transfer widths: 1 B (< 255 levels, above), 2 B (< 65535 levels) and the
     # full 4 B copy for deeper traversals; pageable outputs work too
-    for n in (600, 70000):
+    # transfer widths: 4-bit codes (< 15 levels, above), then ...
+    for n in (100, 600, 70000):
         pg = make_path(n)
         pdg = pg.device(0, 8)
         srcs = [0, n - 1, n // 3]
@@ -332,7 +334,7 @@ def test_batch_api_overlapped_copies(force, slots, port, monkeypatch):
             assert np.array_equal(o, want_s)
             levels = int(want_s.max()) + 1  # a path is connected
             if force == "8":
-                assert w == (1 if levels < 255 else 2 if levels < 65535 else 4)
+                assert w == (0.5 if levels < 15 else 1 if levels < 255 else 2 if levels < 65535 else 4)
         pg.release_device()
 
 
