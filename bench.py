@@ -761,8 +761,8 @@ def run_single(args):
                 "d2h_bytes_per_step": int(sum(widths) * n),
                 "note": "pbfs_bfs_batch C-ABI call over the 64 sources: every distance array "
                         "copied to pinned host memory (two rotating buffers) while the next "
-                        "traversal runs -- from 2^25 vertices as 1 B/vertex level codes "
-                        "widened to uint32 by host threads; median of steps; L2 flushed "
+                        "traversal runs -- from 2^25 vertices as 4-bit (< 15 levels) or 1-2 B "
+                        "level codes widened to uint32 by host threads; median of steps; L2 flushed "
                         "before each batch",
                 "transfer_bytes_per_vertex": sorted(set(widths)),
                 "batch_ms_per_source": round(t_batch * 1e3, 3),
