@@ -503,3 +503,30 @@ def test_single_call_into_pageable_memory_packed(port, monkeypatch):
         p.device(0, 8).bfs(0, pb.KernelConfig(variant=V.Hybrid, force_top_down_only=True),
                            out=out, want_trace=False)
         assert np.array_equal(out, np.arange(n, dtype=np.uint32))
+    # Code widths at ragged sizes (n not a multiple of the 32-vertex nibble
+    # group or the 16-entry widening step), through a misaligned destination,
+    # with unreached vertices: 4-bit codes (< 15 levels) and 1 B codes (a
+    # 40-level path glued on), single calls and a batch.
+    for n, m, tail in ((3001, 9000, 0), (4097, 20000, 0), (1531, 5000, 40)):
+        rg = random_graph(n, m, seed=n)
+        if tail:
+            pairs = np.column_stack([np.repeat(np.arange(n, dtype=np.int64),
+                                               np.diff(rg.row_offsets).astype(np.int64)),
+                                     rg.column_indices.astype(np.int64)])
+            chain = np.column_stack([np.arange(n - 1, n - 1 + tail), np.arange(n, n + tail)])
+            rg = pb.build_csr(np.vstack([pairs, chain]), n + tail, True, drop_self_loops=True)
+        rdg = rg.device(0, 8)
+        srcs = [int(x) for x in pb.pick_sources(rg, 3, 5)]
+        want = {s: port.bfs_serial(rg.row_offsets, rg.column_indices, s) for s in srcs}
+        for s in srcs:
+            backing = np.empty(rg.vertex_count + 2, dtype=np.uint32)
+            out = backing[2:]  # 8 B past the allocation's alignment: a scalar prologue, then the vector loop
+            rdg.bfs(s, pb.KernelConfig(variant=V.Hybrid), out=out, want_trace=False)
+            assert np.array_equal(out, want[s]), (n, s)
+        outs = [np.empty(rg.vertex_count, np.uint32) for _ in srcs]
+        widths = []
+        rdg.bfs_batch(srcs, pb.KernelConfig(variant=V.Hybrid), outs, widths)
+        for s, o, w in zip(srcs, outs, widths):
+            assert np.array_equal(o, want[s]), (n, s)
+            levels = int(want[s][want[s] != 0xFFFFFFFF].max()) + 1
+            assert w == (0.5 if levels < 15 else 1), (n, s, levels, w)
