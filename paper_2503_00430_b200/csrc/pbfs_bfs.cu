@@ -53,7 +53,7 @@ unsigned widen_threads() {
   return t;
 }
 
-// Host-side widening of packed distances (1 or 2 B per vertex, all-ones =
+// Host-side widening of packed distances (4-bit, 1 B or 2 B codes, all-ones =
 // unreached) into the caller's uint32 arrays, on a persistent pool. Jobs are
 // numbered by the caller (0, 1, 2, ...), submitted in order and run one at a
 // time, each split across every worker.
@@ -877,16 +877,24 @@ pbfs_status pbfs_bfs_locked(pbfs_graph* g, uint32_t source, const pbfs_config* c
   cudaError_t e;
   // A large PAGEABLE destination (e.g. a std::vector behind the reference's
   // KernelFn) would take the driver's staged pageable copy at 4 B/vertex:
-  // instead the kernel also writes 1-2 B/vertex level codes, those land in
-  // pinned staging, and the widening pool expands them into the caller's
-  // array on every host core (faulting its pages in parallel too).
+  // instead the kernel also writes level codes (4 bits to 2 B per vertex),
+  // those land in pinned staging, and the widening pool expands them into the
+  // caller's array on every host core (faulting its pages in parallel too).
+  // A PINNED destination takes the same path only from 2^27 vertices: a lone
+  // call wakes an idle pool, whose widening of a 256 MB array takes ~4 ms
+  // (1.8 ms back to back) and gives back what the shorter transfer saves
+  // (RMAT-26: 146 packed, 150 GTEPS plain), but at 1 GB per array it wins
+  // (RMAT-28: 199 against 141-150; profiles/r02/ab.txt).
+  // PBFS_PINNED_PACKED_MIN=N overrides the vertex count (A/B knob).
   bool packed = false;
   if (dist_host && (g->n >= kPackMinVertices || (g->force & kForcePack))) {
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, dist_host) == cudaSuccess &&
                         pa.type != cudaMemoryTypeUnregistered;
     cudaGetLastError();
-    if (!pinned) {
+    uint64_t pinned_min = uint64_t{1} << 27;
+    if (const char* pm = std::getenv("PBFS_PINNED_PACKED_MIN")) pinned_min = std::strtoull(pm, nullptr, 0);
+    if (!pinned || g->n >= pinned_min) {
       const uint64_t pbytes = ((g->n + 15) / 16) * 32;
       if (!g->pack1 && (st = dalloc(g, &g->pack1, pbytes)) != PBFS_OK) return st;
       if (!g->stage1) PBFS_CUDA(cudaHostAlloc(&g->stage1, pbytes, cudaHostAllocDefault), "pinned staging");
@@ -1034,12 +1042,12 @@ pbfs_status pbfs_bfs_batch(pbfs_graph* g, const uint32_t* sources, uint32_t coun
   // Pipeline per source i (slot = i % S; dist buffer i & 1):
   //   compute stream: traversal i into dist/pack[slot] (+ a narrow copy of
   //                   the distances at the end), control snapshot;
-  //   copy stream:    pack[slot] -> pinned stage[slot] (1 or 2 B/vertex,
+  //   copy stream:    pack[slot] -> pinned stage[slot] (4 bits, 1 B or 2 B per vertex,
   //                   chosen from the level count), then a host callback
   //                   hands it to the widener pool, which writes dist_host[i];
   //   host:           enqueues traversal i+1 before it waits for traversal i.
-  // PCIe then moves n B per source instead of 4n B, overlapped with the next
-  // traversal, and the widening runs on the host cores in parallel.
+  // PCIe then moves n/2 .. 2n B per source instead of 4n B, overlapped with the
+  // next traversal, and the widening runs on the host cores in parallel.
   uint32_t* buf[2] = {g->dist, g->dist2};
   // Narrow transfers pay off once the 4 B/vertex copy outlasts the traversal
   // and the host-side widening (measured: RMAT-26 4.84 -> 3.47 ms per source;
